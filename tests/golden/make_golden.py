@@ -1,0 +1,237 @@
+"""Generate golden vectors from the REFERENCE implementation (alertsim).
+
+Run in the build container, where /root/reference exists:
+    python tests/golden/make_golden.py
+Writes tests/golden/golden_runs.npz and tests/golden/golden_predict.npz.
+The reference is imported read-only from /root/reference/pkg/src; nothing at
+test time reads /root/reference — only these committed fixtures.
+"""
+
+from __future__ import annotations
+
+import json
+import random
+import sys
+from dataclasses import replace
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+sys.path.insert(0, "/root/reference/pkg/tests")
+sys.dont_write_bytecode = True
+
+import alertsim.simulator as S  # noqa: E402
+from alertsim.estimator import KalmanConfig, idle_power_init, slowdown_init  # noqa: E402
+from alertsim.model import ConstraintSpec, DnnKind, Mode, space_to_dict  # noqa: E402
+from alertsim.policies import AlertPolicy, make_policy  # noqa: E402
+from alertsim.predictor import normal_quantile, predict_all  # noqa: E402
+from alertsim.selector import brute_force_select, select  # noqa: E402
+from alertsim.simulator import (  # noqa: E402
+    Constant, EnvironmentPhase, Gaussian, LogNormal, Trace, Uniform, realize, run,
+)
+from alertsim.synth import ProfileKnobs, generate_space, preset_space, preset_trace, reference_latency  # noqa: E402
+from conftest import random_space, random_spec  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def cand_index(space, i, j, target):
+    c = 0
+    for di, d in enumerate(space.dnns):
+        for pj in range(len(space.powers)):
+            targets = [None] if d.kind is DnnKind.TRADITIONAL else list(range(1, len(d.stages) + 1))
+            for t in targets:
+                if (di, pj, t) == (i, j, target):
+                    return c
+                c += 1
+    raise KeyError
+
+
+class Recording:
+    """Wraps a reference policy to capture filter state after every observe."""
+
+    def __init__(self, inner):
+        self.inner = inner
+        self.name = inner.name
+        self.states = []
+
+    def begin(self, space, spec, env):
+        self.inner.begin(space, spec, env)
+
+    def decide(self, index, t_goal):
+        return self.inner.decide(index, t_goal)
+
+    def observe(self, record):
+        self.inner.observe(record)
+        if isinstance(self.inner, AlertPolicy):
+            e, i = self.inner.est, self.inner.idle
+            self.states.append((e.mu, e.sigma2, e.k_gain, e.q_noise, e.last_innovation, i.phi, i.m_var))
+        else:
+            self.states.append((np.nan,) * 7)
+
+
+def run_case(space, spec, trace, policy_name, kalman=None, env=None):
+    env = env if env is not None else realize(trace)
+    orig = S.realize
+    S.realize = lambda tr: env
+    try:
+        pol = Recording(make_policy(policy_name, kalman=kalman))
+        res = run(space, spec, trace, pol)
+    finally:
+        S.realize = orig
+    recs = res.records
+    out = {
+        "cand": np.array([cand_index(space, r.decision.dnn_index, r.decision.power_index,
+                                     r.decision.target_stage) for r in recs], np.int32),
+        "level": np.array([["none", "dropped-energy", "dropped-accuracy"].index(r.decision.fallback_level.value)
+                           for r in recs], np.int32),
+        "completed": np.array([r.completed_stage for r in recs], np.int32),
+        "met": np.array([r.deadline_met for r in recs], np.int32),
+        "viol": np.array([(r.violations.latency, r.violations.accuracy, r.violations.energy) for r in recs],
+                         np.int32),
+        "period": np.array([r.period for r in recs]),
+        "latency": np.array([r.observed_latency for r in recs]),
+        "accuracy": np.array([r.delivered_accuracy for r in recs]),
+        "energy": np.array([r.energy for r in recs]),
+        "fb": np.array([(r.fb_latency, r.fb_t_prof) for r in recs]),
+        "state": np.array(pol.states),
+        "s": np.asarray(env.slowdown, np.float64),
+        "idle": np.asarray(env.idle_power, np.float64),
+        "phase": np.asarray(env.phase_index, np.int32),
+        "summary": np.array([res.summary.mean_energy, res.summary.mean_accuracy,
+                             res.summary.violation_rates["latency"], res.summary.violation_rates["accuracy"],
+                             res.summary.violation_rates["energy"]]),
+        "phase_summary": np.array([[p.length, p.mean_energy, p.mean_accuracy, p.violation_rates["latency"],
+                                    p.violation_rates["accuracy"], p.violation_rates["energy"]]
+                                   for p in res.summary.per_phase]),
+    }
+    return out
+
+
+def spec_json(spec, group_size=None):
+    return {"mode": spec.mode.value, "t_goal": spec.t_goal, "e_goal": spec.e_goal, "q_goal": spec.q_goal,
+            "pr_threshold": spec.pr_threshold, "overhead_budget": spec.overhead_budget,
+            "group_size": group_size}
+
+
+def kalman_json(k):
+    return None if k is None else {f: getattr(k, f) for f in
+                                   ("k0", "r", "q0", "alpha", "mu0", "sigma2_0", "sigma2_uses_current_gain")}
+
+
+def random_trace(rnd, n):
+    phases = []
+    left = n
+    while left > 0:
+        L = min(left, rnd.randint(5, max(6, n // 2)))
+        kind = rnd.choice(["c", "g", "l", "u"])
+        if kind == "c":
+            d = Constant(rnd.uniform(0.5, 2.5))
+        elif kind == "g":
+            d = Gaussian(rnd.uniform(0.6, 2.0), rnd.uniform(0.01, 0.5))
+        elif kind == "l":
+            d = LogNormal(rnd.uniform(-0.3, 0.8), rnd.uniform(0.05, 0.5))
+        else:
+            lo = rnd.uniform(0.3, 1.5)
+            d = Uniform(lo, lo + rnd.uniform(0.1, 1.5))
+        phases.append(EnvironmentPhase(L, d, rnd.uniform(1.0, 12.0), rnd.choice([0.0, 0.05, 0.2])))
+        left -= L
+    return Trace(seed=rnd.randint(0, 10**6), phases=tuple(phases[:8]),
+                 group_size=rnd.choice([None, None, None, rnd.randint(1, 6)]))
+
+
+def main():
+    cases = []  # (name, space, spec, trace, policy, kalman)
+    space = preset_space()
+    ref = reference_latency(space)
+    tr600 = preset_trace()
+    c1 = ConstraintSpec(mode=Mode.MINIMIZE_ENERGY, t_goal=0.14, q_goal=0.68, overhead_budget=0.01 * ref)
+    for pol in ("alert", "alert-any", "alert-trad", "oracle"):
+        cases.append((f"preset600_minE_{pol}", space, c1, tr600, pol, None))
+    tmax = 0.8 * ref
+    cmax = ConstraintSpec(mode=Mode.MAXIMIZE_ACCURACY, t_goal=tmax, e_goal=0.6 * 50.0 * tmax,
+                          pr_threshold=0.95, overhead_budget=0.01 * ref)
+    for pol in ("alert", "alert-any", "oracle"):
+        cases.append((f"preset600_maxA_pr95_{pol}", space, cmax, tr600, pol, None))
+    tr1000 = Trace(seed=42, phases=tuple(
+        EnvironmentPhase(n, p.slowdown_dist, p.idle_power_true, p.input_noise_sd)
+        for n, p in zip((334, 333, 333), tr600.phases)))
+    for dm in (0.4, 0.8, 1.2, 1.6, 2.0):
+        for q in (0.70, 0.85):
+            sp = ConstraintSpec(mode=Mode.MINIMIZE_ENERGY, t_goal=dm * ref, q_goal=q, overhead_budget=0.01 * ref)
+            cases.append((f"c1_1000_dm{dm}_q{q}", space, sp, tr1000, "alert", None))
+        for em in (0.5, 0.8):
+            sp = ConstraintSpec(mode=Mode.MAXIMIZE_ACCURACY, t_goal=dm * ref, e_goal=em * 50.0 * dm * ref,
+                                pr_threshold=0.95 if dm != 1.2 else None, overhead_budget=0.01 * ref)
+            cases.append((f"c1_1000_dm{dm}_e{em}", space, sp, tr1000, "alert", None))
+    trg = replace(preset_trace(phase_length=40), group_size=4)
+    cases.append(("group4_minE", space, c1, trg, "alert", None))
+    cases.append(("group4_minE_oracle", space, c1, trg, "oracle", None))
+    cases.append(("kalman_variant", space, c1, preset_trace(phase_length=50), "alert",
+                  KalmanConfig(q0=0.02, r=0.01, alpha=0.5, sigma2_uses_current_gain=True)))
+    # large table (64 x 32, 2,144 candidates), short trace
+    big = generate_space(ProfileKnobs(n_dnns=64, n_powers=32))
+    bref = reference_latency(big)
+    bsp = ConstraintSpec(mode=Mode.MINIMIZE_ENERGY, t_goal=1.0 * bref, q_goal=0.8, overhead_budget=0.01 * bref)
+    btr = preset_trace(phase_length=20)
+    cases.append(("big64x32_minE_alert", big, bsp, btr, "alert", None))
+    cases.append(("big64x32_minE_oracle", big, bsp, btr, "oracle", None))
+    bsp2 = ConstraintSpec(mode=Mode.MAXIMIZE_ACCURACY, t_goal=0.8 * bref, e_goal=0.6 * 50.0 * 0.8 * bref,
+                          pr_threshold=0.95, overhead_budget=0.01 * bref)
+    cases.append(("big64x32_maxA_alert", big, bsp2, btr, "alert", None))
+    # randomized spaces / specs / traces (reference conftest generators)
+    rnd = random.Random(20261017)
+    for k in range(24):
+        rs = random_space(rnd)
+        spc = random_spec(rnd)
+        spc = replace(spc, overhead_budget=rnd.choice([0.0, 0.01 * spc.t_goal]))
+        tr = random_trace(rnd, 80)
+        pol = ["alert", "oracle", "alert-any", "alert-trad"][k % 4]
+        if pol == "alert-any" and not any(d.kind is DnnKind.ANYTIME for d in rs.dnns):
+            pol = "alert"
+        if pol == "alert-trad" and not any(d.kind is DnnKind.TRADITIONAL for d in rs.dnns):
+            pol = "alert"
+        cases.append((f"random{k:02d}_{pol}", rs, spc, tr, pol, None))
+
+    arrays = {}
+    meta = []
+    for name, sp, spec, tr, pol, kal in cases:
+        out = run_case(sp, spec, tr, pol, kal)
+        for key, val in out.items():
+            arrays[f"{name}/{key}"] = val
+        meta.append({"name": name, "space": space_to_dict(sp), "spec": spec_json(spec, tr.group_size),
+                     "policy": pol, "kalman": kalman_json(kal), "n_phases": len(tr.phases)})
+        print(name, "E", out["summary"][0], "acc", out["summary"][1])
+    arrays["meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+    np.savez_compressed(OUT / "golden_runs.npz", **arrays)
+
+    # predict_all / select / brute_force_select on random instances (conftest.py:74-82)
+    rnd = random.Random(987654)
+    pmeta, parr = [], {}
+    for k in range(300):
+        rs = random_space(rnd)
+        spc = random_spec(rnd)
+        est = replace(slowdown_init(), mu=rnd.uniform(0.3, 3.0), sigma2=rnd.uniform(0.0, 0.6))
+        if k % 10 == 0:
+            est = replace(est, sigma2=0.0)
+        idle = replace(idle_power_init(0.5), phi=rnd.uniform(0.0, 1.0))
+        goal = spc.t_goal * rnd.choice([1.0, 0.5, 1.3])
+        preds = predict_all(rs, est, idle, spc, goal)
+        d = select(preds, spc)
+        b = brute_force_select(preds, spc)
+        parr[f"{k}/pred"] = np.array([(p.pr_deadline, p.expected_accuracy, p.energy, p.latency_mean,
+                                       p.latency_sigma) for p in preds])
+        parr[f"{k}/sel"] = np.array([cand_index(rs, d.dnn_index, d.power_index, d.target_stage),
+                                     ["none", "dropped-energy", "dropped-accuracy"].index(d.fallback_level.value),
+                                     cand_index(rs, b.dnn_index, b.power_index, b.target_stage)], np.int32)
+        pmeta.append({"space": space_to_dict(rs), "spec": spec_json(spc), "mu": est.mu, "sigma2": est.sigma2,
+                      "phi": idle.phi, "goal": goal,
+                      "z_q": normal_quantile(spc.pr_threshold) if spc.pr_threshold is not None else None})
+    parr["meta"] = np.frombuffer(json.dumps(pmeta).encode(), np.uint8)
+    np.savez_compressed(OUT / "golden_predict.npz", **parr)
+
+
+if __name__ == "__main__":
+    main()
