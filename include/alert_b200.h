@@ -73,7 +73,7 @@ enum { ALERT_DTYPE_F32 = 0, ALERT_DTYPE_F64 = 1 };
 /* Compiled limits */
 #define ALERT_MAX_STAGES 8         /* stages per anytime DNN                   */
 #define ALERT_MAX_PHASES 8         /* phase ids per trace for per-phase sums   */
-#define ALERT_MAX_CANDIDATES 16384
+#define ALERT_MAX_CANDIDATES 6144   /* 32 B/candidate of shared memory per block */
 
 /* ---- candidate table (host description) -------------------------------- */
 /* Flattened model.ConfigSpace (model.py:55-63).  Stages are stored dnn-major;
@@ -131,6 +131,9 @@ typedef struct AlertTrace {
   int64_t n_steps;            /* steps available per row                       */
   int64_t row_stride;         /* elements between rows  (time-major: 1)        */
   int64_t step_stride;        /* elements between steps (time-major: n_rows)   */
+  int64_t step_offset;        /* first step held by `slowdown` (chunked streaming:
+                                 element (row, n) is at (n - step_offset) * step_stride
+                                 + row * row_stride); 0 for a whole trace        */
   int32_t max_segments;       /* per-row capacity of the segment arrays        */
   int32_t _pad;
   const int32_t* n_segments;  /* [n_rows]                                      */
@@ -185,12 +188,14 @@ enum {
  *   bits 27..29 phase id                                                   */
 typedef struct AlertOutputs {
   uint32_t* decision;
-  float* energy;        /* StepRecord.energy                 */
-  float* accuracy;      /* StepRecord.delivered_accuracy     */
-  float* latency;       /* StepRecord.observed_latency       */
-  float* mu;            /* slow-down mean after observe      */
-  float* sigma2;        /* slow-down variance after observe  */
+  void* energy;         /* StepRecord.energy                 */
+  void* accuracy;       /* StepRecord.delivered_accuracy     */
+  void* latency;        /* StepRecord.observed_latency       */
+  void* mu;             /* slow-down mean after observe      */
+  void* sigma2;         /* slow-down variance after observe  */
   uint32_t* oracle_decision; /* ALERT_POLICY_ALERT_WITH_ORACLE only */
+  int32_t record_dtype; /* ALERT_DTYPE_F32 (default) or ALERT_DTYPE_F64 for the five value arrays */
+  int32_t _pad;
   int64_t stream_stride;
   int64_t step_stride;
   double* agg;          /* [n_streams][ALERT_AGG_FIELDS] or NULL */
@@ -272,6 +277,10 @@ int alert_get_launch(AlertContext* ctx, int* lanes_per_stream, int* threads_per_
 
 /* Number of alert_* kernels launched through this context (instrumentation). */
 int64_t alert_launch_count(AlertContext* ctx);
+
+/* Measured FP32 issue peak (FFMA lane-ops/s) of a device: the denominator of
+ * the FP32 roofline (instrumentation, not part of the scheduling path). */
+int alert_probe_fp32_peak(int device, double* slots_per_s);
 
 #ifdef __cplusplus
 }

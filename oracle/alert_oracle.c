@@ -677,7 +677,7 @@ static void* batch_worker(void* arg) {
     int64_t row = t->stream_row ? t->stream_row[k] : k;
     for (int64_t n = 0; n < len; ++n) {
       int64_t step = J->step_begin + n;
-      int64_t off = row * t->row_stride + step * t->step_stride;
+      int64_t off = row * t->row_stride + (step - t->step_offset) * t->step_stride;
       sd[n] = t->slowdown_dtype == ALERT_DTYPE_F64 ? ((const double*)t->slowdown)[off]
                                                    : (double)((const float*)t->slowdown)[off];
       int seg = 0;

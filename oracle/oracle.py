@@ -185,7 +185,7 @@ def host_trace_struct(packed, stream_row=None):
         slowdown=packed.slowdown.ctypes.data,
         slowdown_dtype=abi.DTYPE_F64 if packed.slowdown.dtype == np.float64 else abi.DTYPE_F32,
         n_rows=packed.n_rows, n_steps=packed.n_steps, row_stride=1, step_stride=packed.n_rows,
-        max_segments=packed.seg_end.shape[1], _pad=0,
+        step_offset=0, max_segments=packed.seg_end.shape[1], _pad=0,
         n_segments=packed.n_segments.ctypes.data, seg_end=packed.seg_end.ctypes.data,
         seg_phase=packed.seg_phase.ctypes.data, seg_idle=packed.seg_idle.ctypes.data,
         stream_row=None if sr is None else sr.ctypes.data,

@@ -17,7 +17,7 @@ FLAG_FP64_ALL = 0x1
 FLAG_NO_REFINE = 0x2
 MAX_STAGES = 8
 MAX_PHASES = 8
-MAX_CANDIDATES = 16384
+MAX_CANDIDATES = 6144
 
 AGG_N, AGG_ENERGY, AGG_ENERGY_C, AGG_ACC, AGG_ACC_C = range(5)
 AGG_VIOL_LAT, AGG_VIOL_ACC, AGG_VIOL_ENERGY = 5, 6, 7
@@ -91,7 +91,7 @@ class AlertTrace(C.Structure):
     _fields_ = [
         ("slowdown", C.c_void_p), ("slowdown_dtype", C.c_int32), ("n_rows", C.c_int32),
         ("n_steps", C.c_int64), ("row_stride", C.c_int64), ("step_stride", C.c_int64),
-        ("max_segments", C.c_int32), ("_pad", C.c_int32),
+        ("step_offset", C.c_int64), ("max_segments", C.c_int32), ("_pad", C.c_int32),
         ("n_segments", C.c_void_p), ("seg_end", C.c_void_p), ("seg_phase", C.c_void_p),
         ("seg_idle", C.c_void_p), ("stream_row", C.c_void_p),
     ]
@@ -112,7 +112,7 @@ class AlertOutputs(C.Structure):
     _fields_ = [
         ("decision", C.c_void_p), ("energy", C.c_void_p), ("accuracy", C.c_void_p),
         ("latency", C.c_void_p), ("mu", C.c_void_p), ("sigma2", C.c_void_p),
-        ("oracle_decision", C.c_void_p),
+        ("oracle_decision", C.c_void_p), ("record_dtype", C.c_int32), ("_pad", C.c_int32),
         ("stream_stride", C.c_int64), ("step_stride", C.c_int64),
         ("agg", C.c_void_p), ("forced", C.c_void_p),
     ]

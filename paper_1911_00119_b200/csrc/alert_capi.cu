@@ -1,0 +1,666 @@
+// alert_capi.cu — kernels and the C ABI (include/alert_b200.h) of the B200
+// ALERT scheduling step.  Build: see __graft_entry__.py (nvcc, sm_100a).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "alert_kernels.cuh"
+
+using namespace alert;
+
+// ==========================================================================
+// error plumbing
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                               \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return fail(ALERT_ERR_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+struct AlertContext {
+  int device = 0;
+  int lanes = 0;  // 0 = auto
+  int tpb = 128;
+  int n_sm = 148;
+  int max_smem = 227 * 1024;
+  std::atomic<long long> launches{0};
+};
+
+struct AlertTable {
+  DevTable dev{};
+  void* buf = nullptr;  // one device allocation holding every array
+  int n_cand = 0;
+  std::vector<int32_t> cand_dnn, cand_power, cand_stage;
+  int n_any_cols = 0;
+  int device = 0;
+};
+
+// ==========================================================================
+// kernels
+
+// predict_all for n streams: out[i][candidate] in reference order, FP64 exact.
+__global__ void predict_kernel(const StepParams P, AlertPrediction* out, const int32_t* cand_dnn,
+                               const int32_t* cand_power, const int32_t* cand_stage) {
+  const long long total = P.n * P.T.n_cells;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long i = g / P.T.n_cells;
+    const int c = (int)(g % P.T.n_cells);  // candidate index
+    const int cell = P.T.cell_of_cand[c];
+    const int si = P.stream_spec ? P.stream_spec[i] : (int)(i % P.n_specs);
+    const AlertSpec spec = P.specs[si];
+    StepCtx x;
+    make_ctx(x, &spec, P.st.mu[i], P.st.sigma2[i], P.st.phi[i], P.goal[i], true);
+    Pred64 q = eval64(P.T, x, cell);
+    AlertPrediction r;
+    double t = P.T.t64[cell];
+    r.latency_mean = xmul(x.mu, t);
+    r.latency_sigma = xmul(x.sig, t);
+    r.pr_deadline = q.pr;
+    r.expected_accuracy = q.acc;
+    r.energy = q.energy;
+    r.dnn_index = cand_dnn[c];
+    r.power_index = cand_power[c];
+    r.target_stage = cand_stage[c];
+    r._pad = 0;
+    out[g] = r;
+  }
+}
+
+__global__ void observe_kernel(const DevTable T, const AlertFilterConfig cfg, AlertState st, const double* fb_lat,
+                               const double* fb_t, const double* idle, const int32_t* power, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Filter f{st.mu[i], st.sigma2[i], st.k_gain[i], st.q_noise[i], st.innov[i], st.phi[i], st.m_var[i]};
+  slowdown_update(cfg, f, fb_lat[i], fb_t[i]);
+  idle_update(cfg, f, idle[i], T.power_cap64[power[i]]);
+  st.mu[i] = f.mu; st.sigma2[i] = f.sigma2; st.k_gain[i] = f.k_gain; st.q_noise[i] = f.q_noise;
+  st.innov[i] = f.innov; st.phi[i] = f.phi; st.m_var[i] = f.m_var;
+}
+
+__global__ void state_init_kernel(AlertState st, AlertFilterConfig cfg, double phi0, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  st.mu[i] = cfg.mu0;  // slowdown_init, estimator.py:47-56
+  st.sigma2[i] = cfg.sigma2_0;
+  st.k_gain[i] = cfg.k0;
+  st.q_noise[i] = cfg.q0;
+  st.innov[i] = 0.0;
+  st.phi[i] = phi0;  // idle_power_init(phi0), policies.py:90-91
+  st.m_var[i] = cfg.m0;
+  st.group_budget[i] = 0.0;
+  st.group_count[i] = 0;
+}
+
+// Deterministic reduction: fixed chunks of streams per block, fixed order.
+constexpr int kReduceChunk = 4096;
+constexpr int kReduceRep = 3;  // threads per field
+__global__ void reduce_partial_kernel(const double* agg, long long n, double* partial) {
+  __shared__ double sh[kReduceRep * ALERT_AGG_FIELDS];
+  const int t = threadIdx.x;  // blockDim = kReduceRep * FIELDS
+  const int field = t % ALERT_AGG_FIELDS, rep = t / ALERT_AGG_FIELDS;
+  const long long s0 = (long long)blockIdx.x * kReduceChunk;
+  const long long s1 = min(n, s0 + kReduceChunk);
+  double acc = 0.0;
+  for (long long s = s0 + rep; s < s1; s += kReduceRep) acc = xadd(acc, agg[s * ALERT_AGG_FIELDS + field]);
+  sh[t] = acc;
+  __syncthreads();
+  if (rep == 0) {
+    double v = sh[field];
+    for (int r = 1; r < kReduceRep; ++r) v = xadd(v, sh[r * ALERT_AGG_FIELDS + field]);
+    partial[(long long)blockIdx.x * ALERT_AGG_FIELDS + field] = v;
+  }
+}
+
+__global__ void reduce_final_kernel(const double* partial, long long nb, double* out) {
+  const int field = threadIdx.x;
+  if (field >= ALERT_AGG_FIELDS) return;
+  double v = 0.0;
+  for (long long b = 0; b < nb; ++b) v = xadd(v, partial[b * ALERT_AGG_FIELDS + field]);
+  out[field] = v;
+}
+
+// ==========================================================================
+// host side
+
+int alert_abi_version(void) { return ALERT_ABI_VERSION; }
+
+const char* alert_strerror(int status) {
+  switch (status) {
+    case ALERT_OK: return "ok";
+    case ALERT_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case ALERT_ERR_INVALID_SPACE: return "invalid config space";
+    case ALERT_ERR_INVALID_SPEC: return "invalid constraint spec";
+    case ALERT_ERR_INVALID_TRACE: return "invalid trace";
+    case ALERT_ERR_CUDA: return "CUDA error";
+    case ALERT_ERR_UNSUPPORTED: return "unsupported size";
+    case ALERT_ERR_NO_CANDIDATE: return "no candidate of the requested kinds";
+    default: return "unknown status";
+  }
+}
+
+const char* alert_last_error(void) { return g_last_error.c_str(); }
+
+int alert_create(AlertContext** out, int device) {
+  if (!out) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_create: out is NULL");
+  int n = 0;
+  CUDA_TRY(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_create: bad device index");
+  CUDA_TRY(cudaSetDevice(device));
+  AlertContext* c = new AlertContext();
+  c->device = device;
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  c->n_sm = prop.multiProcessorCount;
+  c->max_smem = (int)prop.sharedMemPerBlockOptin;
+  *out = c;
+  return ALERT_OK;
+}
+
+int alert_destroy(AlertContext* ctx) {
+  delete ctx;
+  return ALERT_OK;
+}
+
+int alert_set_launch(AlertContext* ctx, int lanes, int tpb) {
+  if (!ctx) return fail(ALERT_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "lanes_per_stream must be 0 or a power of two <= 32");
+  if (tpb != 0 && (tpb < 32 || tpb > 256 || tpb % 32))
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "threads_per_block must be a multiple of 32 in [32, 256]");
+  ctx->lanes = lanes;
+  ctx->tpb = tpb ? tpb : 128;
+  return ALERT_OK;
+}
+
+int alert_get_launch(AlertContext* ctx, int* lanes, int* tpb) {
+  if (!ctx) return fail(ALERT_ERR_INVALID_ARGUMENT, "ctx is NULL");
+  if (lanes) *lanes = ctx->lanes;
+  if (tpb) *tpb = ctx->tpb;
+  return ALERT_OK;
+}
+
+int64_t alert_launch_count(AlertContext* ctx) { return ctx ? (int64_t)ctx->launches.load() : -1; }
+
+// model.validate (model.py:100-163), first problem only
+static std::string validate_space(const AlertSpaceDesc* d) {
+  char buf[256];
+  if (d->n_powers < 1) return "power axis is empty";
+  if (d->n_dnns < 1) return "DNN axis is empty";
+  if (!(d->p_idle_prof > 0)) return "p_idle_prof must be positive";
+  double prev = 0.0;
+  for (int j = 0; j < d->n_powers; ++j) {
+    if (!(d->power_cap[j] > prev)) {
+      snprintf(buf, sizeof buf, "power[%d]: cap %g W not strictly above previous", j, d->power_cap[j]);
+      return buf;
+    }
+    prev = d->power_cap[j];
+  }
+  int off = 0;
+  for (int i = 0; i < d->n_dnns; ++i) {
+    int ns = d->dnn_n_stages[i];
+    int kind = d->dnn_kind[i];
+    if (kind != ALERT_KIND_TRADITIONAL && kind != ALERT_KIND_ANYTIME) return "unknown DNN kind";
+    if (kind == ALERT_KIND_TRADITIONAL && ns != 1) return "traditional profile must have exactly 1 stage";
+    if (kind == ALERT_KIND_ANYTIME && ns < 2) return "anytime profile needs >= 2 stages";
+    if (ns > ALERT_MAX_STAGES) return "too many stages (ALERT_MAX_STAGES)";
+    double qf = d->dnn_q_fail[i];
+    if (!(qf >= 0.0 && qf <= 1.0)) return "q_fail outside [0,1]";
+    if (qf > d->stage_accuracy[off]) return "q_fail exceeds first-stage accuracy";
+    double pa = -1.0;
+    for (int k = 0; k < ns; ++k) {
+      double a = d->stage_accuracy[off + k];
+      if (!(a >= 0.0 && a <= 1.0)) return "stage accuracy outside [0,1]";
+      if (kind == ALERT_KIND_ANYTIME && a <= pa) return "anytime accuracies not increasing";
+      pa = a;
+      const double* t = d->stage_t_prof + (size_t)(off + k) * d->n_powers;
+      for (int j = 0; j < d->n_powers; ++j) {
+        if (!(t[j] > 0)) return "latency not positive";
+        if (j > 0 && t[j] > t[j - 1]) return "latency increases with the power cap";
+        if (kind == ALERT_KIND_ANYTIME && k > 0 && t[j] <= t[j - d->n_powers])
+          return "anytime stage latencies not strictly increasing";
+      }
+    }
+    off += ns;
+  }
+  return "";
+}
+
+int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** out) {
+  if (!ctx || !d || !out) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_table_create: NULL argument");
+  if (!d->dnn_kind || !d->dnn_n_stages || !d->dnn_q_fail || !d->stage_accuracy || !d->stage_t_prof || !d->power_cap)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_table_create: NULL array in AlertSpaceDesc");
+  std::string prob = validate_space(d);
+  if (!prob.empty()) return fail(ALERT_ERR_INVALID_SPACE, "invalid profile: " + prob);
+  const int P = d->n_powers;
+  std::vector<int> stage_off(d->n_dnns);
+  int off = 0;
+  for (int i = 0; i < d->n_dnns; ++i) { stage_off[i] = off; off += d->dnn_n_stages[i]; }
+  // candidate enumeration (policies.py:59-67) and the cell order (traditional first)
+  AlertTable* tb = new AlertTable();
+  std::vector<int> trad_cells, any_cells;  // values = candidate index
+  std::vector<int2> cols;
+  int c = 0;
+  for (int i = 0; i < d->n_dnns; ++i)
+    for (int j = 0; j < P; ++j) {
+      bool trad = d->dnn_kind[i] == ALERT_KIND_TRADITIONAL;
+      int nt = trad ? 1 : d->dnn_n_stages[i];
+      for (int k = 0; k < nt; ++k, ++c) {
+        tb->cand_dnn.push_back(i);
+        tb->cand_power.push_back(j);
+        tb->cand_stage.push_back(trad ? 0 : k + 1);
+        (trad ? trad_cells : any_cells).push_back(c);
+      }
+    }
+  const int n = c;
+  if (n > ALERT_MAX_CANDIDATES || P > 1023 || d->n_dnns > 4095) {
+    delete tb;
+    return fail(ALERT_ERR_UNSUPPORTED, "table too large for the packed tie-break key / shared memory");
+  }
+  std::vector<int> order(trad_cells);
+  for (size_t q = 0; q < any_cells.size();) {  // columns of consecutive stages
+    int cand = any_cells[q];
+    int ns = d->dnn_n_stages[tb->cand_dnn[cand]];
+    cols.push_back(make_int2((int)order.size(), ns));
+    for (int k = 0; k < ns; ++k) order.push_back(any_cells[q + k]);
+    q += ns;
+  }
+  std::vector<float4> A(n), B(n);
+  std::vector<double> t64(n), a64(n), qf64(n), cap64(n);
+  std::vector<int> cell_of_cand(n);
+  double max_cap = d->power_cap[P - 1];
+  for (int cell = 0; cell < n; ++cell) {
+    int cand = order[cell];
+    int i = tb->cand_dnn[cand], j = tb->cand_power[cand], st = tb->cand_stage[cand];
+    int k0 = st == 0 ? 0 : st - 1;
+    double t = d->stage_t_prof[(size_t)(stage_off[i] + k0) * P + j];
+    double a = d->stage_accuracy[stage_off[i] + k0];
+    double qf = d->dnn_q_fail[i];
+    double prev = k0 == 0 ? qf : d->stage_accuracy[stage_off[i] + k0 - 1];
+    uint32_t key = ((uint32_t)j << 20) | ((uint32_t)i << 8) | (uint32_t)st;
+    A[cell] = make_float4((float)(1.0 / t), (float)t, (float)d->power_cap[j], (float)(a - prev));
+    float kb, cb, sb;
+    memcpy(&kb, &key, 4);
+    memcpy(&cb, &cand, 4);
+    memcpy(&sb, &st, 4);
+    B[cell] = make_float4((float)qf, kb, cb, sb);
+    t64[cell] = t;
+    a64[cell] = a;
+    qf64[cell] = qf;
+    cap64[cell] = d->power_cap[j];
+    cell_of_cand[cand] = cell;
+  }
+  size_t bytes = 0;
+  auto place = [&](size_t sz) { size_t o = (bytes + 255) & ~size_t(255); bytes = o + sz; return o; };
+  size_t oA = place(sizeof(float4) * n), oB = place(sizeof(float4) * n), oC = place(sizeof(int2) * (cols.size() + 1));
+  size_t oT = place(8 * n), oAcc = place(8 * n), oQ = place(8 * n), oCap = place(8 * n), oCell = place(4 * n);
+  size_t oPw = place(8 * P);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  char* buf = nullptr;
+  cudaError_t e = cudaMalloc(&buf, bytes);
+  if (e != cudaSuccess) {
+    delete tb;
+    return fail(ALERT_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  std::vector<char> h(bytes, 0);
+  memcpy(&h[oA], A.data(), sizeof(float4) * n);
+  memcpy(&h[oB], B.data(), sizeof(float4) * n);
+  if (!cols.empty()) memcpy(&h[oC], cols.data(), sizeof(int2) * cols.size());
+  memcpy(&h[oT], t64.data(), 8 * n);
+  memcpy(&h[oAcc], a64.data(), 8 * n);
+  memcpy(&h[oQ], qf64.data(), 8 * n);
+  memcpy(&h[oCap], cap64.data(), 8 * n);
+  memcpy(&h[oCell], cell_of_cand.data(), 4 * n);
+  memcpy(&h[oPw], d->power_cap, 8 * P);
+  e = cudaMemcpy(buf, h.data(), bytes, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(buf);
+    delete tb;
+    return fail(ALERT_ERR_CUDA, std::string("cudaMemcpy: ") + cudaGetErrorString(e));
+  }
+  DevTable& T = tb->dev;
+  T.n_cells = n;
+  T.n_trad = (int)trad_cells.size();
+  T.n_any_cols = (int)cols.size();
+  T.n_powers = P;
+  T.cellA = reinterpret_cast<const float4*>(buf + oA);
+  T.cellB = reinterpret_cast<const float4*>(buf + oB);
+  T.any_cols = reinterpret_cast<const int2*>(buf + oC);
+  T.t64 = reinterpret_cast<const double*>(buf + oT);
+  T.a64 = reinterpret_cast<const double*>(buf + oAcc);
+  T.qf64 = reinterpret_cast<const double*>(buf + oQ);
+  T.cap64 = reinterpret_cast<const double*>(buf + oCap);
+  T.cell_of_cand = reinterpret_cast<const int*>(buf + oCell);
+  double r = d->p_idle_prof / max_cap;
+  T.phi0 = (1.0 < r) ? 1.0 : r;  // min(1.0, p_idle_prof / max cap), policies.py:90
+  T.power_cap64 = reinterpret_cast<const double*>(buf + oPw);
+  tb->buf = buf;
+  tb->n_cand = n;
+  tb->n_any_cols = (int)cols.size();
+  tb->device = ctx->device;
+  *out = tb;
+  return ALERT_OK;
+}
+
+int alert_table_destroy(AlertTable* tb) {
+  if (!tb) return ALERT_OK;
+  cudaSetDevice(tb->device);
+  cudaFree(tb->buf);
+  delete tb;
+  return ALERT_OK;
+}
+
+int alert_table_num_candidates(const AlertTable* tb) { return tb ? tb->n_cand : -1; }
+
+int alert_table_candidate(const AlertTable* tb, int c, int32_t* dnn, int32_t* power, int32_t* stage) {
+  if (!tb || c < 0 || c >= tb->n_cand) return fail(ALERT_ERR_INVALID_ARGUMENT, "candidate index out of range");
+  if (dnn) *dnn = tb->cand_dnn[c];
+  if (power) *power = tb->cand_power[c];
+  if (stage) *stage = tb->cand_stage[c];
+  return ALERT_OK;
+}
+
+// ConstraintSpec invariants (model.py:81-97) + group size
+static int check_specs(const AlertSpec* specs, int n) {
+  if (!specs || n < 1) return fail(ALERT_ERR_INVALID_ARGUMENT, "specs: need at least one spec");
+  for (int k = 0; k < n; ++k) {
+    const AlertSpec& s = specs[k];
+    char where[64];
+    snprintf(where, sizeof where, "spec[%d]: ", k);
+    if (s.mode != ALERT_MODE_MIN_ENERGY && s.mode != ALERT_MODE_MAX_ACCURACY)
+      return fail(ALERT_ERR_INVALID_SPEC, std::string(where) + "unknown mode");
+    if (!(s.overhead_budget >= 0)) return fail(ALERT_ERR_INVALID_SPEC, std::string(where) + "overhead_budget must be >= 0");
+    if (!(s.t_goal > s.overhead_budget))
+      return fail(ALERT_ERR_INVALID_SPEC, std::string(where) + "t_goal must exceed overhead_budget");
+    if (s.mode == ALERT_MODE_MAX_ACCURACY && !(s.e_goal > 0))
+      return fail(ALERT_ERR_INVALID_SPEC, std::string(where) + "e_goal must be positive");
+    if (s.mode == ALERT_MODE_MIN_ENERGY && !(s.q_goal > 0))
+      return fail(ALERT_ERR_INVALID_SPEC, std::string(where) + "q_goal must be positive");
+    if (s.has_pr && !(s.pr_threshold > 0.0 && s.pr_threshold < 1.0))
+      return fail(ALERT_ERR_INVALID_SPEC, std::string(where) + "pr_threshold must lie in (0, 1)");
+    if (s.group_size < 0) return fail(ALERT_ERR_INVALID_SPEC, std::string(where) + "group_size must be >= 0");
+  }
+  return ALERT_OK;
+}
+
+static int kinds_of(int policy, const AlertTable* tb) {
+  int k = policy == ALERT_POLICY_ALERT_ANY ? 2 : policy == ALERT_POLICY_ALERT_TRAD ? 1 : 3;
+  int have = (tb->dev.n_trad > 0 ? 1 : 0) | (tb->dev.n_any_cols > 0 ? 2 : 0);
+  return (k & have) ? k : 0;
+}
+
+static size_t table_smem(const AlertTable* tb) {
+  return sizeof(float4) * 2 * (size_t)tb->dev.n_cells + sizeof(int2) * (size_t)(tb->dev.n_any_cols + 1);
+}
+
+static size_t run_smem(const AlertTable* tb, int tpb, int W) {
+  size_t base = (table_smem(tb) + 15) & ~size_t(15);
+  return base + sizeof(TileAgg) * (size_t)(tpb / W);
+}
+
+static int pick_lanes(const AlertContext* ctx, const AlertTable* tb) {
+  if (ctx->lanes) return ctx->lanes;
+  return tb->n_cand <= 256 ? 1 : 32;
+}
+
+// Upload host specs to stream-ordered device memory (freed after the launch).
+static int upload_specs(const AlertSpec* specs, int n, cudaStream_t st, AlertSpec** dev) {
+  CUDA_TRY(cudaMallocAsync((void**)dev, sizeof(AlertSpec) * n, st));
+  CUDA_TRY(cudaMemcpyAsync(*dev, specs, sizeof(AlertSpec) * n, cudaMemcpyHostToDevice, st));
+  return ALERT_OK;
+}
+
+static int dispatch_run(int W, int pf, const RunParams& P, int tpb, size_t smem, cudaStream_t st) {
+  cudaError_t e;
+  switch (W) {
+    case 1: e = launch_run<1>(pf, P, tpb, smem, st); break;
+    case 2: e = launch_run<2>(pf, P, tpb, smem, st); break;
+    case 4: e = launch_run<4>(pf, P, tpb, smem, st); break;
+    case 8: e = launch_run<8>(pf, P, tpb, smem, st); break;
+    case 16: e = launch_run<16>(pf, P, tpb, smem, st); break;
+    default: e = launch_run<32>(pf, P, tpb, smem, st); break;
+  }
+  if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("run_kernel: ") + cudaGetErrorString(e));
+  return ALERT_OK;
+}
+
+int alert_state_init(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* cfg, AlertState st,
+                     int64_t n, void* cuda_stream) {
+  if (!ctx || !tb || !cfg) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_state_init: NULL argument");
+  if (n < 0) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_state_init: n < 0");
+  if (!st.mu || !st.sigma2 || !st.k_gain || !st.q_noise || !st.innov || !st.phi || !st.m_var || !st.group_budget ||
+      !st.group_count)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_state_init: NULL state array");
+  if (n == 0) return ALERT_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  state_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(st, *cfg, tb->dev.phi0, n);
+  CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return ALERT_OK;
+}
+
+int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* cfg, const AlertSpec* specs,
+              int32_t n_specs, const int32_t* stream_spec, const AlertTrace* tr, AlertState st,
+              const AlertOutputs* out, int32_t policy, uint32_t flags, int64_t stream_begin, int64_t stream_end,
+              int64_t step_begin, int64_t step_end, void* cuda_stream) {
+  if (!ctx || !tb || !cfg || !tr || !out) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: NULL argument");
+  int r = check_specs(specs, n_specs);
+  if (r) return r;
+  if (policy < ALERT_POLICY_ALERT || policy > ALERT_POLICY_ALERT_WITH_ORACLE)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: unknown policy");
+  int kinds = kinds_of(policy, tb);
+  if (!kinds) return fail(ALERT_ERR_NO_CANDIDATE, "alert_run: space has no DNN of the policy's kinds");
+  if (!tr->slowdown || !tr->n_segments || !tr->seg_end || !tr->seg_phase || !tr->seg_idle || tr->max_segments < 1)
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_run: incomplete trace description");
+  if (tr->slowdown_dtype != ALERT_DTYPE_F32 && tr->slowdown_dtype != ALERT_DTYPE_F64)
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_run: unknown slowdown dtype");
+  if (step_begin < tr->step_offset || step_end < step_begin || step_end > tr->step_offset + tr->n_steps)
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_run: step range outside the trace buffer");
+  if (stream_begin < 0 || stream_end < stream_begin)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: bad stream range");
+  if (!tr->stream_row && stream_end > tr->n_rows)
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_run: more streams than trace rows and no stream_row map");
+  if (!st.mu || !st.sigma2 || !st.k_gain || !st.q_noise || !st.innov || !st.phi || !st.m_var || !st.group_budget ||
+      !st.group_count)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: NULL state array");
+  if ((out->decision || out->energy || out->accuracy || out->latency || out->mu || out->sigma2 ||
+       out->oracle_decision || out->forced) &&
+      (out->stream_stride == 0 && out->step_stride == 0))
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: per-step outputs need strides");
+  if (stream_end == stream_begin || step_end == step_begin) return ALERT_OK;
+  int W = pick_lanes(ctx, tb);
+  size_t smem = run_smem(tb, ctx->tpb, W);
+  if ((int)smem > ctx->max_smem) return fail(ALERT_ERR_UNSUPPORTED, "alert_run: table exceeds shared memory");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  AlertSpec* dspecs = nullptr;
+  r = upload_specs(specs, n_specs, s, &dspecs);
+  if (r) return r;
+  RunParams P;
+  P.T = tb->dev;
+  P.cfg = *cfg;
+  P.specs = dspecs;
+  P.n_specs = n_specs;
+  P.stream_spec = stream_spec;
+  P.tr = *tr;
+  P.st = st;
+  P.out = *out;
+  P.policy = policy;
+  P.flags = flags;
+  P.kinds = kinds;
+  P.stream_begin = stream_begin;
+  P.stream_end = stream_end;
+  P.step_begin = step_begin;
+  P.step_end = step_end;
+  int pf = policy == ALERT_POLICY_ORACLE ? PF_ORACLE : policy == ALERT_POLICY_ALERT_WITH_ORACLE ? PF_BOTH : PF_ALERT;
+  r = dispatch_run(W, pf, P, ctx->tpb, smem, s);
+  cudaFreeAsync(dspecs, s);
+  if (r) return r;
+  ctx->launches++;
+  return ALERT_OK;
+}
+
+int alert_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs, int32_t n_specs,
+                 const int32_t* stream_spec, AlertState st, const double* plan_goal, int32_t policy, uint32_t flags,
+                 uint32_t* decision, int64_t n, void* cuda_stream) {
+  if (!ctx || !tb || !plan_goal || !decision) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_decide: NULL argument");
+  int r = check_specs(specs, n_specs);
+  if (r) return r;
+  if (policy < ALERT_POLICY_ALERT || policy > ALERT_POLICY_ALERT_TRAD)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_decide: policy must be alert, alert-any or alert-trad");
+  int kinds = kinds_of(policy, tb);
+  if (!kinds) return fail(ALERT_ERR_NO_CANDIDATE, "alert_decide: space has no DNN of the policy's kinds");
+  if (n <= 0) return n < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_decide: n < 0") : ALERT_OK;
+  size_t smem = table_smem(tb);
+  if ((int)smem > ctx->max_smem) return fail(ALERT_ERR_UNSUPPORTED, "alert_decide: table exceeds shared memory");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  AlertSpec* dspecs = nullptr;
+  r = upload_specs(specs, n_specs, s, &dspecs);
+  if (r) return r;
+  StepParams P{};
+  P.T = tb->dev;
+  P.specs = dspecs;
+  P.n_specs = n_specs;
+  P.stream_spec = stream_spec;
+  P.st = st;
+  P.goal = plan_goal;
+  P.policy = policy;
+  P.flags = flags;
+  P.kinds = kinds;
+  P.n = n;
+  cudaError_t e;
+  switch (pick_lanes(ctx, tb)) {
+    case 1: e = launch_decide<1>(P, decision, ctx->tpb, smem, s); break;
+    case 2: e = launch_decide<2>(P, decision, ctx->tpb, smem, s); break;
+    case 4: e = launch_decide<4>(P, decision, ctx->tpb, smem, s); break;
+    case 8: e = launch_decide<8>(P, decision, ctx->tpb, smem, s); break;
+    case 16: e = launch_decide<16>(P, decision, ctx->tpb, smem, s); break;
+    default: e = launch_decide<32>(P, decision, ctx->tpb, smem, s); break;
+  }
+  if (e != cudaSuccess) r = fail(ALERT_ERR_CUDA, std::string("decide_kernel: ") + cudaGetErrorString(e));
+  cudaFreeAsync(dspecs, s);
+  if (r) return r;
+  ctx->launches++;
+  return ALERT_OK;
+}
+
+int alert_predict(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs, int32_t n_specs,
+                  const int32_t* stream_spec, AlertState st, const double* plan_goal, AlertPrediction* out,
+                  int64_t n, void* cuda_stream) {
+  if (!ctx || !tb || !plan_goal || !out) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_predict: NULL argument");
+  int r = check_specs(specs, n_specs);
+  if (r) return r;
+  if (n <= 0) return n < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_predict: n < 0") : ALERT_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  AlertSpec* dspecs = nullptr;
+  r = upload_specs(specs, n_specs, s, &dspecs);
+  if (r) return r;
+  // per-candidate (dnn, power, stage) arrays in stream-ordered scratch
+  int nc = tb->n_cand;
+  int32_t* meta = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&meta, sizeof(int32_t) * 3 * nc, s));
+  CUDA_TRY(cudaMemcpyAsync(meta, tb->cand_dnn.data(), 4 * nc, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(meta + nc, tb->cand_power.data(), 4 * nc, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(meta + 2 * nc, tb->cand_stage.data(), 4 * nc, cudaMemcpyHostToDevice, s));
+  StepParams P{};
+  P.T = tb->dev;
+  P.specs = dspecs;
+  P.n_specs = n_specs;
+  P.stream_spec = stream_spec;
+  P.st = st;
+  P.goal = plan_goal;
+  P.n = n;
+  long long total = n * nc;
+  unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 65535LL * 4);
+  predict_kernel<<<blocks, 256, 0, s>>>(P, out, meta, meta + nc, meta + 2 * nc);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(meta, s);
+  cudaFreeAsync(dspecs, s);
+  if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("predict_kernel: ") + cudaGetErrorString(e));
+  ctx->launches++;
+  return ALERT_OK;
+}
+
+int alert_observe(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* cfg, AlertState st,
+                  const double* fb_latency, const double* fb_t_prof, const double* idle, const int32_t* power,
+                  int64_t n, void* cuda_stream) {
+  if (!ctx || !tb || !cfg || !fb_latency || !fb_t_prof || !idle || !power)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_observe: NULL argument");
+  if (n <= 0) return n < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_observe: n < 0") : ALERT_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  observe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(tb->dev, *cfg, st, fb_latency, fb_t_prof, idle, power, n);
+  CUDA_TRY(cudaGetLastError());
+  ctx->launches++;
+  return ALERT_OK;
+}
+
+int alert_oracle_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs, int32_t n_specs,
+                        const int32_t* stream_spec, const double* sd, const double* idle, const double* plan_goal,
+                        uint32_t flags, uint32_t* decision, int64_t n, void* cuda_stream) {
+  (void)flags;
+  if (!ctx || !tb || !sd || !idle || !plan_goal || !decision)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_oracle_decide: NULL argument");
+  int r = check_specs(specs, n_specs);
+  if (r) return r;
+  if (n <= 0) return n < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_oracle_decide: n < 0") : ALERT_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  AlertSpec* dspecs = nullptr;
+  r = upload_specs(specs, n_specs, s, &dspecs);
+  if (r) return r;
+  int W = pick_lanes(ctx, tb);
+  int tpb = ctx->tpb;
+  unsigned blocks = (unsigned)((n * W + tpb - 1) / tpb);
+  cudaError_t e;
+  switch (W) {
+    case 1: e = launch_oracle<1>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
+    case 2: e = launch_oracle<2>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
+    case 4: e = launch_oracle<4>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
+    case 8: e = launch_oracle<8>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
+    case 16: e = launch_oracle<16>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
+    default: e = launch_oracle<32>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
+  }
+  cudaFreeAsync(dspecs, s);
+  if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("oracle_decide_kernel: ") + cudaGetErrorString(e));
+  ctx->launches++;
+  return ALERT_OK;
+}
+
+int alert_reduce(AlertContext* ctx, const double* agg, int64_t n, double* out, void* cuda_stream) {
+  if (!ctx || !agg || !out) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_reduce: NULL argument");
+  if (n < 0) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_reduce: n < 0");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  long long nb = (n + kReduceChunk - 1) / kReduceChunk;
+  if (nb == 0) {
+    CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * ALERT_AGG_FIELDS, s));
+    return ALERT_OK;
+  }
+  double* partial = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&partial, sizeof(double) * ALERT_AGG_FIELDS * nb, s));
+  reduce_partial_kernel<<<(unsigned)nb, kReduceRep * ALERT_AGG_FIELDS, 0, s>>>(agg, n, partial);
+  reduce_final_kernel<<<1, 128, 0, s>>>(partial, nb, out);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(partial, s);
+  if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("reduce: ") + cudaGetErrorString(e));
+  ctx->launches += 2;
+  return ALERT_OK;
+}
+

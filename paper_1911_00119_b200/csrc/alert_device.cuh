@@ -1,0 +1,596 @@
+// alert_device.cuh — device side of the B200 ALERT scheduling step.
+//
+// One "tile" of W lanes (W = 1..32, a cooperative-groups partition of a warp)
+// owns one stream.  Per step the tile
+//   1. adjusts the goal                 selector.py:48-70, simulator.py:473-483
+//   2. scans every candidate in FP32    predictor.py:147-197 + selector.py:102-131
+//      (Phi via erff on the FMA/MUFU pipes, running top-2 per fallback level,
+//      constraint-boundary uncertainty), lanes striding over candidates,
+//      then merges lanes with shuffles;
+//   3. re-ranks in FP64 — with the reference's exact formulas and operation
+//      order — only when the FP32 top-2 gap or a constraint margin is inside
+//      the FP32 error bound (near-tie), so decisions equal the FP64 reference;
+//   4. executes / measures / observes in FP64   simulator.py:249-382,
+//      estimator.py:59-127, keeping the filter state in registers.
+//
+// Candidates are stored as "cells" (one per (dnn, power, target stage)); the
+// table is reordered so traditional cells come first (flat loop) and anytime
+// DNNs follow as columns of consecutive stages (the telescoping expected
+// accuracy, predictor.py:100-108, becomes a running FMA along the column).
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cstdint>
+#include <math_constants.h>
+
+#include "../../include/alert_b200.h"
+
+namespace alert {
+
+namespace cg = cooperative_groups;
+
+constexpr float kInfF = __builtin_huge_valf();
+constexpr double kInf = __builtin_huge_val();
+constexpr float kEps = 1.1920929e-07f;  // 2^-23
+constexpr double kSqrt2 = 1.4142135623730951;  // math.sqrt(2.0), predictor.py:21
+
+// --------------------------------------------------------------------------
+// device table
+struct DevTable {
+  int n_cells;      // == number of candidates
+  int n_trad;       // cells [0, n_trad) are traditional, one per (dnn, power)
+  int n_any_cols;   // anytime columns (dnn, power) after the traditional cells
+  int n_powers;
+  const float4* cellA;    // {1/t, t, cap, d = a_k - a_{k-1} (a_0 = q_fail)}
+  const float4* cellB;    // {q_fail, key bits, candidate index bits, stage bits}
+  const int2* any_cols;   // {first cell, number of stages}
+  const double* t64;      // profiled latency of the cell's stage at its power
+  const double* a64;      // stage accuracy
+  const double* qf64;     // q_fail of the cell's dnn
+  const double* cap64;    // power cap of the cell's power setting
+  const int* cell_of_cand;
+  const double* power_cap64;  // [n_powers] caps by power index
+  double phi0;            // min(1, p_idle_prof / max cap), policies.py:90
+};
+
+// Exact FP64 helpers: no FMA contraction, Python's min/max semantics.
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
+__device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
+
+// Neumaier step exactly as CPython 3.12 sum() (bltinmodule.c).
+__device__ __forceinline__ void neumaier(double& s, double& c, double x) {
+  double t = xadd(s, x);
+  if (fabs(s) >= fabs(x))
+    c = xadd(c, xadd(xsub(s, t), x));
+  else
+    c = xadd(c, xadd(xsub(x, t), s));
+  s = t;
+}
+
+// Standard normal CDF, FP32 (predictor.py:25-27 in single precision).
+__device__ __forceinline__ float phi32(float z) {
+  return fmaf(0.5f, erff(z * 0.70710678118654752f), 0.5f);
+}
+
+// deadline_probability, exact reference arithmetic (predictor.py:48-65).
+__device__ __forceinline__ double phi64(double goal, double mu, double sig, double t) {
+  double mean = xmul(mu, t);
+  double sd = xmul(sig, t);
+  if (sd == 0.0) return mean <= goal ? 1.0 : 0.0;
+  double x = xdiv(xsub(goal, mean), sd);
+  return xmul(0.5, xadd(1.0, erf(xdiv(x, kSqrt2))));
+}
+
+// --------------------------------------------------------------------------
+// per-step context shared by the lanes of a tile
+struct StepCtx {
+  // FP64 state (exact path)
+  double mu, sig, phi, goal, zq;
+  const AlertSpec* spec;
+  // FP32 scan inputs
+  float goal_f, mu_f, inv_sig, mu_e, omp, phig;
+  // FP32 error bounds
+  float d_pr, d_acc, d_erel;
+  // thresholds with margins
+  float q_hi, q_lo, th_hi, th_lo, e_hi, e_lo;
+  bool fp64_all;
+};
+
+__device__ __forceinline__ void make_ctx(StepCtx& x, const AlertSpec* sp, double mu, double sigma2,
+                                         double phi, double goal, bool fp64_all) {
+  x.spec = sp;
+  x.mu = mu;
+  x.sig = sqrt(sigma2);  // sigma2 ** 0.5 (estimator.py:42-44)
+  x.phi = phi;
+  x.goal = goal;
+  x.zq = sp->z_q;
+  x.goal_f = (float)goal;
+  x.mu_f = (float)mu;
+  float sig_f = (float)x.sig;
+  x.inv_sig = 1.0f / sig_f;
+  double mu_e = sp->has_pr ? xadd(mu, xmul(sp->z_q, x.sig)) : mu;  // predictor.py:140
+  x.mu_e = (float)mu_e;
+  float phi_f = (float)phi;
+  x.omp = 1.0f - phi_f;
+  x.phig = phi_f * x.goal_f;
+  float r = fabsf(x.mu_f) * x.inv_sig;
+  // |dPhi| <= eps*(0.625 + 0.6*mu/sigma) from rounding of z, + erff / blend error,
+  // times a safety factor of 2.
+  x.d_pr = 2.0f * kEps * (0.625f + 0.6f * r + 2.0f);
+  x.d_acc = x.d_pr + 8.0f * kEps;
+  x.d_erel = 12.0f * kEps;
+  x.fp64_all = fp64_all || !(sig_f > 0.0f) || !isfinite(x.inv_sig) || !isfinite(x.d_pr) ||
+               !(fabs(mu_e) < 1e30);
+  x.q_hi = (float)sp->q_goal + x.d_acc;
+  x.q_lo = (float)sp->q_goal - x.d_acc;
+  x.th_hi = (float)sp->pr_threshold + x.d_pr;
+  x.th_lo = (float)sp->pr_threshold - x.d_pr;
+  x.e_hi = (float)sp->e_goal * (1.0f - x.d_erel);  // sure: E <= e_hi
+  x.e_lo = (float)sp->e_goal * (1.0f + x.d_erel);  // possible: E <= e_lo
+}
+
+// --------------------------------------------------------------------------
+// FP32 running top-2 per fallback level
+struct Tracker {
+  float b1, b2, un;
+  int i1;
+  __device__ __forceinline__ void init() { b1 = b2 = un = kInfF; i1 = -1; }
+  __device__ __forceinline__ void push(float v, bool sure, bool unc, int c) {
+    float vs = sure ? v : kInfF;
+    b2 = fminf(b2, fmaxf(b1, vs));
+    if (vs < b1) i1 = c;
+    b1 = fminf(b1, vs);
+    un = fminf(un, unc ? v : kInfF);
+  }
+  template <class Tile>
+  __device__ __forceinline__ void merge(const Tile& tile) {
+#pragma unroll
+    for (int m = 1; m < Tile::num_threads(); m <<= 1) {
+      float ob1 = tile.shfl_xor(b1, m), ob2 = tile.shfl_xor(b2, m), oun = tile.shfl_xor(un, m);
+      int oi = tile.shfl_xor(i1, m);
+      b2 = fminf(fminf(b2, ob2), fmaxf(b1, ob1));
+      if (ob1 < b1 || (ob1 == b1 && (unsigned)oi < (unsigned)i1)) i1 = oi;
+      b1 = fminf(b1, ob1);
+      un = fminf(un, oun);
+    }
+  }
+};
+
+// FP64 lexicographic key (selector.py:87-91 / policies.py:142-146)
+struct Key64 {
+  double p0, p1;
+  uint32_t tk;
+  int cell;
+  __device__ __forceinline__ void init() { p0 = p1 = kInf; tk = 0xFFFFFFFFu; cell = -1; }
+  __device__ __forceinline__ bool less(const Key64& o) const {
+    if (p0 != o.p0) return p0 < o.p0;
+    if (p1 != o.p1) return p1 < o.p1;
+    return tk < o.tk;
+  }
+  template <class Tile>
+  __device__ __forceinline__ void merge(const Tile& tile) {
+#pragma unroll
+    for (int m = 1; m < Tile::num_threads(); m <<= 1) {
+      Key64 o;
+      o.p0 = tile.shfl_xor(p0, m);
+      o.p1 = tile.shfl_xor(p1, m);
+      o.tk = tile.shfl_xor(tk, m);
+      o.cell = tile.shfl_xor(cell, m);
+      if (o.cell >= 0 && (cell < 0 || o.less(*this))) *this = o;
+    }
+  }
+};
+
+// --------------------------------------------------------------------------
+// FP64 exact prediction of one cell (predict_all, predictor.py:147-197)
+struct Pred64 {
+  double pr, acc, energy;
+};
+
+__device__ __forceinline__ Pred64 eval64(const DevTable& T, const StepCtx& x, int c) {
+  Pred64 r;
+  float4 B = T.cellB[c];
+  int stage = __float_as_int(B.w);  // 0 = traditional
+  double t = T.t64[c];
+  double qf = T.qf64[c];
+  r.pr = phi64(x.goal, x.mu, x.sig, t);
+  if (stage == 0) {
+    r.acc = xadd(xmul(r.pr, T.a64[c]), xmul(xsub(1.0, r.pr), qf));  // accuracy_blend
+  } else {
+    // expected_accuracy_anytime (predictor.py:100-108), reference order,
+    // streaming prs[m], prs[m+1] instead of materialising the list
+    int first = c - (stage - 1);
+    double p_cur = stage == 1 ? r.pr : phi64(x.goal, x.mu, x.sig, T.t64[first]);
+    double acc = xmul(xsub(1.0, p_cur), qf);
+    for (int m = 0; m < stage; ++m) {
+      double p_next = (m + 1 == stage) ? 0.0
+                      : (m + 2 == stage) ? r.pr
+                                         : phi64(x.goal, x.mu, x.sig, T.t64[first + m + 1]);
+      acc = xadd(acc, xmul(T.a64[first + m], xsub(p_cur, p_next)));
+      p_cur = p_next;
+    }
+    r.acc = acc;
+  }
+  double p = T.cap64[c];
+  if (x.spec->has_pr) {  // predict_energy_percentile, predictor.py:129-144
+    double lat = xmul(xadd(x.mu, xmul(x.zq, x.sig)), t);
+    double idle = py_max(0.0, xsub(x.goal, py_min(lat, x.goal)));
+    r.energy = xadd(xmul(p, lat), xmul(xmul(x.phi, p), idle));
+  } else {  // predict_energy_mean, predictor.py:111-126
+    double lat = xmul(x.mu, t);
+    r.energy = xadd(xmul(p, lat), xmul(xmul(x.phi, p), py_max(0.0, xsub(x.goal, lat))));
+  }
+  return r;
+}
+
+// feasibility at a fallback level (selector.py:73-84, _LEVELS :94-99)
+__device__ __forceinline__ bool feasible64(const StepCtx& x, const Pred64& p, int level) {
+  const AlertSpec* s = x.spec;
+  if (level < 2 && s->has_pr && p.pr < s->pr_threshold) return false;
+  if (s->mode == ALERT_MODE_MAX_ACCURACY) return level != 0 || p.energy <= s->e_goal;
+  return level == 2 || p.acc >= s->q_goal;
+}
+
+__device__ __forceinline__ Key64 key64(const StepCtx& x, const Pred64& p, int level, uint32_t tk, int c) {
+  Key64 k;
+  bool acc_mode = level == 2 || x.spec->mode == ALERT_MODE_MAX_ACCURACY;
+  k.p0 = acc_mode ? -p.acc : p.energy;
+  k.p1 = acc_mode ? p.energy : -p.acc;
+  k.tk = tk;
+  k.cell = c;
+  return k;
+}
+
+// --------------------------------------------------------------------------
+// The decision: FP32 scan, FP64 re-rank of near-ties.
+struct Decision {
+  int cell;
+  int level;
+  bool refined;
+};
+
+// Level-l objective in FP32: min-energy L0 -> E (relative bound), otherwise -acc.
+template <int MODE>
+__device__ __forceinline__ bool energy_objective(int level) {
+  return MODE == ALERT_MODE_MIN_ENERGY && level == 0;
+}
+
+template <int MODE, bool HAS_PR>
+struct AlertScan {
+  Tracker t[3];
+  // refine-pass state
+  int level;
+  float cut;
+  bool all;
+  Key64 best;
+
+  // FP32 classification of a cell at a level: sure / possible, objective value
+  __device__ __forceinline__ void classify(const StepCtx& x, int lvl, float pr, float acc, float E,
+                                           bool& sure, bool& poss, float& v) const {
+    bool pr_s = !HAS_PR || lvl == 2 || pr >= x.th_hi;
+    bool pr_p = !HAS_PR || lvl == 2 || pr >= x.th_lo;
+    if (MODE == ALERT_MODE_MIN_ENERGY) {
+      if (lvl == 2) { sure = true; poss = true; }
+      else { sure = pr_s && acc >= x.q_hi; poss = pr_p && acc >= x.q_lo; }
+    } else {
+      if (lvl == 0) { sure = pr_s && E <= x.e_hi; poss = pr_p && E <= x.e_lo; }
+      else { sure = pr_s; poss = pr_p; }
+    }
+    v = energy_objective<MODE>(lvl) ? E : -acc;
+  }
+
+  __device__ __forceinline__ void scan_cell(const StepCtx& x, int c, float pr, float acc, float E) {
+    bool s, p;
+    float v;
+    classify(x, 0, pr, acc, E, s, p, v);
+    t[0].push(v, s, p && !s, c);
+    if (MODE == ALERT_MODE_MAX_ACCURACY) {
+      classify(x, 1, pr, acc, E, s, p, v);
+      t[1].push(v, s, p && !s, c);
+    }
+    if (MODE == ALERT_MODE_MIN_ENERGY || HAS_PR) t[2].push(-acc, true, false, c);
+  }
+
+  __device__ __forceinline__ void refine_cell(const DevTable& T, const StepCtx& x, int c, float pr,
+                                              float acc, float E, uint32_t tk) {
+    bool relevant = all;
+    if (!relevant) {
+      bool s, p;
+      float v;
+      classify(x, level, pr, acc, E, s, p, v);
+      relevant = p && v <= cut;
+    }
+    if (!relevant) return;
+    Pred64 q = eval64(T, x, c);
+    if (!feasible64(x, q, level)) return;
+    Key64 k = key64(x, q, level, tk, c);
+    if (best.cell < 0 || k.less(best)) best = k;
+  }
+};
+
+template <int MODE>
+__device__ __forceinline__ float cutoff(const StepCtx& x, int level, float b1) {
+  if (!(b1 < kInfF)) return kInfF;
+  if (energy_objective<MODE>(level)) return b1 + fabsf(b1) * (4.0f * x.d_erel) + 1e-30f;
+  return b1 + 2.0f * x.d_acc;
+}
+
+// One pass over the cells (PASS 0 = FP32 scan, 1 = refine at scan.level).
+template <int PASS, int MODE, bool HAS_PR, class Tile>
+__device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __restrict__ sA,
+                                          const float4* __restrict__ sB, const int2* __restrict__ sCol,
+                                          const Tile& tile, const StepCtx& x, int kinds,
+                                          AlertScan<MODE, HAS_PR>& S) {
+  const int W = Tile::num_threads();
+  const int lane = tile.thread_rank();
+  const bool skip32 = PASS == 1 && S.all;
+  if (kinds & 1) {
+    for (int c = lane; c < T.n_trad; c += W) {
+      float4 A = sA[c];
+      float pr = 0.f, acc = 0.f, E = 0.f;
+      if (!skip32) {
+        float qf = sB[c].x;
+        pr = phi32(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig);
+        acc = fmaf(pr, A.w, qf);
+        float lat = x.mu_e * A.y;
+        E = A.z * fmaxf(lat, fmaf(x.omp, lat, x.phig));
+      }
+      if (PASS == 0) S.scan_cell(x, c, pr, acc, E);
+      else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
+    }
+  }
+  if (kinds & 2) {
+    for (int col = lane; col < T.n_any_cols; col += W) {
+      int2 cd = sCol[col];
+      float acc = sB[cd.x].x;
+      for (int k = 0; k < cd.y; ++k) {
+        int c = cd.x + k;
+        float4 A = sA[c];
+        float pr = 0.f, E = 0.f;
+        if (!skip32) {
+          pr = phi32(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig);
+          acc = fmaf(pr, A.w, acc);
+          float lat = x.mu_e * A.y;
+          E = A.z * fmaxf(lat, fmaf(x.omp, lat, x.phig));
+        }
+        if (PASS == 0) S.scan_cell(x, c, pr, acc, E);
+        else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
+      }
+    }
+  }
+}
+
+// AlertPolicy.decide (policies.py:97-103) for the tile's stream.
+template <int MODE, bool HAS_PR, class Tile>
+__device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const float4* sB,
+                                   const int2* sCol, const Tile& tile, const StepCtx& x, int kinds,
+                                   bool no_refine) {
+  AlertScan<MODE, HAS_PR> S;
+#pragma unroll
+  for (int l = 0; l < 3; ++l) S.t[l].init();
+  // fallback levels that can be distinct (selector.py:94-99): min-energy L1 == L0;
+  // max-accuracy without pr_threshold: L1 admits everything, L2 unreachable.
+  constexpr int NL = (MODE == ALERT_MODE_MIN_ENERGY) ? 2 : (HAS_PR ? 3 : 2);
+  Decision d{-1, 0, false};
+  int start = 0;
+  if (!x.fp64_all) {
+    cell_pass<0>(T, sA, sB, sCol, tile, x, kinds, S);
+#pragma unroll
+    for (int l = 0; l < 3; ++l) S.t[l].merge(tile);
+    start = -1;
+    bool done = false;
+#pragma unroll
+    for (int li = 0; li < NL; ++li) {
+      const int L = (li == 1 && MODE == ALERT_MODE_MIN_ENERGY) ? 2 : li;
+      const Tracker& tr = S.t[L];
+      if (!done) {
+        float cut = cutoff<MODE>(x, L, tr.b1);
+        if (tr.un < kInfF && (!(tr.b1 < kInfF) || tr.un <= cut)) {
+          start = li;
+          done = true;
+        } else if (tr.b1 < kInfF) {
+          if (tr.b2 <= cut) start = li;
+          else { d.cell = tr.i1; d.level = L; }
+          done = true;
+        }
+      }
+    }
+    if (start < 0) return d;
+    if (no_refine) {  // FP32-only decision (measurement mode, not reference-exact)
+#pragma unroll
+      for (int li = 0; li < NL; ++li) {
+        const int L = (li == 1 && MODE == ALERT_MODE_MIN_ENERGY) ? 2 : li;
+        if (li >= start && d.cell < 0 && S.t[L].b1 < kInfF) { d.cell = S.t[L].i1; d.level = L; }
+      }
+      return d;
+    }
+  }
+  // FP64 re-rank, level by level from the first uncertain one
+#pragma unroll
+  for (int li = 0; li < NL; ++li) {
+    const int L = (li == 1 && MODE == ALERT_MODE_MIN_ENERGY) ? 2 : li;
+    if (li >= start && d.cell < 0) {
+      S.level = L;
+      S.all = x.fp64_all;
+      S.cut = x.fp64_all ? kInfF : cutoff<MODE>(x, L, S.t[L].b1);
+      S.best.init();
+      cell_pass<1>(T, sA, sB, sCol, tile, x, kinds, S);
+      S.best.merge(tile);
+      if (S.best.cell >= 0) {
+        d.cell = S.best.cell;
+        d.level = L;
+        d.refined = true;
+      }
+    }
+  }
+  return d;
+}
+
+template <class Tile>
+__device__ __forceinline__ Decision alert_decide(const DevTable& T, const float4* sA, const float4* sB,
+                                                 const int2* sCol, const Tile& tile, const StepCtx& x,
+                                                 int kinds, bool no_refine) {
+  if (x.spec->mode == ALERT_MODE_MIN_ENERGY) {
+    if (x.spec->has_pr) return alert_decide_t<ALERT_MODE_MIN_ENERGY, true>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+    return alert_decide_t<ALERT_MODE_MIN_ENERGY, false>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+  }
+  if (x.spec->has_pr) return alert_decide_t<ALERT_MODE_MAX_ACCURACY, true>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+  return alert_decide_t<ALERT_MODE_MAX_ACCURACY, false>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+}
+
+// --------------------------------------------------------------------------
+// execute_decision + measure (simulator.py:249-280, 329-382), FP64
+struct Outcome {
+  double latency;    // StepRecord.observed_latency (incl. overhead tax)
+  double delivered;  // delivered accuracy
+  double energy;
+  double fb_latency, fb_t_prof;
+  int completed;
+  bool met, vl, va, ve;
+};
+
+__device__ __forceinline__ Outcome execute_measure(const DevTable& T, const AlertSpec* sp, int c, double s,
+                                                   double goal, double period, double idle) {
+  Outcome o;
+  int stage = __float_as_int(T.cellB[c].w);
+  double lat;
+  if (stage == 0) {
+    double t = T.t64[c];
+    lat = xmul(s, t);
+    o.completed = lat <= goal ? 1 : 0;
+    o.fb_latency = lat;
+    o.fb_t_prof = t;
+  } else {
+    int first = c - (stage - 1);
+    double stop = py_min(xmul(s, T.t64[c]), goal);
+    int completed = 0;
+    for (int m = 0; m < stage; ++m)
+      if (xmul(s, T.t64[first + m]) <= stop) completed = m + 1;
+    o.completed = completed;
+    lat = stop;
+    if (completed) {
+      double t = T.t64[first + completed - 1];
+      o.fb_latency = xmul(s, t);
+      o.fb_t_prof = t;
+    } else {
+      o.fb_latency = stop;
+      o.fb_t_prof = T.t64[first];
+    }
+  }
+  double cap = T.cap64[c];
+  o.latency = xadd(lat, sp->overhead_budget);
+  if (o.completed >= 1) {
+    int first = stage == 0 ? c : c - (stage - 1);
+    o.delivered = T.a64[first + o.completed - 1];
+  } else {
+    o.delivered = T.qf64[c];
+  }
+  o.met = o.completed >= 1 && o.latency <= period;
+  o.energy = xadd(xmul(cap, py_min(o.latency, period)), xmul(idle, py_max(0.0, xsub(period, o.latency))));
+  o.vl = !o.met;
+  o.va = sp->mode == ALERT_MODE_MIN_ENERGY && o.delivered < sp->q_goal;
+  o.ve = sp->mode == ALERT_MODE_MAX_ACCURACY && o.energy > sp->e_goal;
+  return o;
+}
+
+// --------------------------------------------------------------------------
+// filters (estimator.py:59-84, 110-127), FP64 in registers
+struct Filter {
+  double mu, sigma2, k_gain, q_noise, innov, phi, m_var;
+};
+
+__device__ __forceinline__ void slowdown_update(const AlertFilterConfig& cfg, Filter& f, double obs, double t_prof) {
+  double ky = xmul(f.k_gain, f.innov);
+  double q = py_max(cfg.q0, xadd(xmul(cfg.alpha, f.q_noise), xmul(xsub(1.0, cfg.alpha), xmul(ky, ky))));
+  double prior = xadd(xmul(xsub(1.0, f.k_gain), f.sigma2), q);
+  double k = xdiv(prior, xadd(prior, cfg.r));
+  double y = xsub(xdiv(obs, t_prof), f.mu);
+  double mu = xadd(f.mu, xmul(k, y));
+  double s2 = cfg.sigma2_uses_current_gain ? xadd(xmul(xsub(1.0, k), f.sigma2), q) : prior;
+  f.mu = mu;
+  f.sigma2 = s2;
+  f.k_gain = k;
+  f.q_noise = q;
+  f.innov = y;
+}
+
+__device__ __forceinline__ void idle_update(const AlertFilterConfig& cfg, Filter& f, double measured, double cap) {
+  double ratio = py_min(1.0, xdiv(measured, cap));
+  double ms = xadd(f.m_var, cfg.s);
+  double w = xdiv(ms, xadd(ms, cfg.v));
+  f.m_var = xmul(xsub(1.0, w), ms);
+  f.phi = xadd(f.phi, xmul(w, xsub(ratio, f.phi)));
+}
+
+// --------------------------------------------------------------------------
+// OraclePolicy.decide (policies.py:160-205): exact per-cell outcome under the
+// true slow-down, three fallback levels at once, FP64.
+template <class Tile>
+__device__ Decision oracle_decide(const DevTable& T, const Tile& tile, const AlertSpec* sp, double s,
+                                  double idle, double goal) {
+  const int W = Tile::num_threads();
+  const int lane = tile.thread_rank();
+  const double oh = sp->overhead_budget;
+  const double period = xadd(goal, oh);
+  const bool maxacc = sp->mode == ALERT_MODE_MAX_ACCURACY;
+  Key64 best[3];
+  best[0].init(); best[1].init(); best[2].init();
+  auto consider = [&](int c, int completed, double lat_raw, double delivered) {
+    double cap = T.cap64[c];
+    double L = xadd(lat_raw, oh);
+    bool met = completed >= 1 && L <= period;
+    double E = xadd(xmul(cap, py_min(L, period)), xmul(idle, py_max(0.0, xsub(period, L))));
+    uint32_t tk = __float_as_uint(T.cellB[c].y);
+#pragma unroll
+    for (int lvl = 0; lvl < 3; ++lvl) {
+      if (lvl != 2 && !met) continue;
+      if (maxacc) {
+        if (lvl == 0 && E > sp->e_goal) continue;
+      } else if (lvl < 2 && delivered < sp->q_goal) {
+        continue;
+      }
+      bool acc_obj = lvl == 2 || maxacc;
+      Key64 k;
+      k.p0 = acc_obj ? -delivered : E;
+      k.p1 = acc_obj ? E : -delivered;
+      k.tk = tk;
+      k.cell = c;
+      if (best[lvl].cell < 0 || k.less(best[lvl])) best[lvl] = k;
+    }
+  };
+  for (int c = lane; c < T.n_trad; c += W) {
+    double lat = xmul(s, T.t64[c]);
+    bool done = lat <= goal;
+    consider(c, done ? 1 : 0, lat, done ? T.a64[c] : T.qf64[c]);
+  }
+  for (int col = lane; col < T.n_any_cols; col += W) {
+    int2 cd = T.any_cols[col];
+    int K = 0;
+    double deliv = T.qf64[cd.x];
+    for (int k = 0; k < cd.y; ++k) {
+      int c = cd.x + k;
+      double st = xmul(s, T.t64[c]);
+      if (st <= goal) { K = k + 1; deliv = T.a64[c]; }
+      consider(c, K, py_min(st, goal), deliv);
+    }
+  }
+  Decision d{-1, 0, true};
+#pragma unroll
+  for (int lvl = 0; lvl < 3; ++lvl) {
+    best[lvl].merge(tile);
+    if (d.cell < 0 && best[lvl].cell >= 0) { d.cell = best[lvl].cell; d.level = lvl; }
+  }
+  return d;
+}
+
+__device__ __forceinline__ uint32_t pack_decision(int cand, int level, const Outcome& o, bool refined, int phase) {
+  return (uint32_t)cand | ((uint32_t)level << 16) | ((uint32_t)o.met << 18) | ((uint32_t)o.vl << 19) |
+         ((uint32_t)o.va << 20) | ((uint32_t)o.ve << 21) | ((uint32_t)(o.completed & 0xF) << 22) |
+         ((uint32_t)refined << 26) | ((uint32_t)(phase & 0x7) << 27);
+}
+
+}  // namespace alert

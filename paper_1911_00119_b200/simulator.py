@@ -1,0 +1,249 @@
+"""Closed-loop runs on the GPU: the drop-in ``run`` and the batched
+``run_batch``.
+
+``run(space, spec, trace, policy)`` has the reference's signature and result
+(simulator.py:461-507) for the policies of :mod:`.policies`, but executes the
+whole trace in ONE launch of the fused kernel (alert_run) instead of a
+Python loop.  ``run_batch`` is the scale-out entry point: many streams
+(scenarios) x many steps per launch, optionally chunked over steps with the
+filter state carried on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import abi
+from .engine import DeviceTrace, Engine, GpuTable, outputs_struct
+from .packing import pack_specs, policy_code
+from .records import (
+    RunResult, StepRecord, Summary, ViolationFlags, decision_of, summary_from_agg,
+)
+from .trace import PackedEnvs, TrueEnvironment, pack_envs, realize
+
+_ENGINES: dict[int, Engine] = {}
+
+
+def get_engine(device: int = 0) -> Engine:
+    e = _ENGINES.get(device)
+    if e is None:
+        e = _ENGINES[device] = Engine(device)
+    return e
+
+
+@dataclass
+class BatchResult:
+    """Outputs of run_batch (host numpy arrays unless keep_on_device)."""
+
+    agg: object                  # [n_streams, AGG_FIELDS] float64
+    state: dict                  # final filter state per stream
+    records: dict = field(default_factory=dict)  # [n_steps, n_streams] per field
+    oracle_decision: object = None
+    candidates: np.ndarray | None = None
+    n_phases: int = abi.MAX_PHASES
+
+    def summaries(self) -> list[Summary]:
+        agg = np.asarray(self.agg)
+        return [summary_from_agg(agg[k], self.n_phases) for k in range(agg.shape[0])]
+
+    def decoded(self) -> dict:
+        return abi.decode_decision(np.asarray(self.records["decision"]).view(np.uint32))
+
+
+def _as_device_trace(engine: Engine, envs, trace_dtype, stream_row) -> DeviceTrace:
+    if isinstance(envs, DeviceTrace):
+        return envs
+    if not isinstance(envs, PackedEnvs):
+        envs = pack_envs(list(envs), dtype=trace_dtype)
+    return engine.upload_trace(envs, stream_row)
+
+
+def run_batch(space, specs: Sequence, envs, policy: str = "alert", *, kalman=None, idle_cfg=None,
+              group_sizes=None, stream_spec=None, stream_row=None, n_streams: int | None = None,
+              records: str | None = None, forced=None, flags: int = 0, chunk_steps: int | None = None,
+              trace_dtype=np.float32, engine: Engine | None = None, device: int = 0,
+              keep_on_device: bool = False, lanes_per_stream: int | None = None) -> BatchResult:
+    """Run ``policy`` over many independent streams in one fused launch.
+
+    specs        ConstraintSpec objects (or an AlertSpec record array); stream k
+                 uses specs[stream_spec[k]] (default k % len(specs)).
+    envs         realized environments (TrueEnvironment-like), a PackedEnvs or
+                 a DeviceTrace; stream k reads row stream_row[k] (default k).
+    records      None (aggregates only), "f32" or "f64" per-step records.
+    forced       [n_steps, n_streams] int32 candidate indices to execute
+                 (teacher forcing; -1 = own decision).
+    """
+    torch = __import__("torch")
+    eng = engine or get_engine(device)
+    if lanes_per_stream is not None:
+        eng.set_launch(lanes_per_stream, 0)
+    table: GpuTable = eng.table(space)
+    spec_arr = specs if isinstance(specs, np.ndarray) and specs.dtype == abi.SPEC_DTYPE \
+        else pack_specs(list(specs), group_sizes)
+    trace = _as_device_trace(eng, envs, trace_dtype, stream_row)
+    if stream_row is not None and trace.stream_row is None:
+        trace.stream_row = torch.as_tensor(np.asarray(stream_row, np.int32)).to(eng.tdev)
+    ns = n_streams if n_streams is not None else (
+        len(stream_row) if stream_row is not None else trace.n_rows)
+    steps = trace.n_steps
+    dev = eng.tdev
+    ss = None
+    if stream_spec is not None:
+        ss = torch.as_tensor(np.asarray(stream_spec, np.int32)).to(dev)
+    state = eng.new_state(table, ns, kalman, idle_cfg)
+    agg = torch.zeros((ns, abi.AGG_FIELDS), dtype=torch.float64, device=dev)
+    rec = {}
+    if records:
+        vdt = torch.float64 if records == "f64" else torch.float32
+        rec["decision"] = torch.empty((steps, ns), dtype=torch.int32, device=dev)
+        for k in ("energy", "accuracy", "latency", "mu", "sigma2"):
+            rec[k] = torch.empty((steps, ns), dtype=vdt, device=dev)
+    pol = policy_code(policy)
+    od = None
+    if pol == abi.POLICY_ALERT_WITH_ORACLE and records:
+        od = torch.empty((steps, ns), dtype=torch.int32, device=dev)
+    fz = None
+    if forced is not None:
+        fz = torch.as_tensor(np.asarray(forced, np.int32)).to(dev)
+        if tuple(fz.shape) != (steps, ns):
+            raise ValueError("forced must be [n_steps, n_streams]")
+    out = outputs_struct(rec, agg=agg, forced=fz, oracle_decision=od)
+    if out.step_stride == 0:
+        out.step_stride, out.stream_stride = ns, 1
+    chunk = chunk_steps or steps
+    for s0 in range(0, steps, chunk):
+        eng.run(table, spec_arr, trace, state, policy=pol, kalman=kalman, idle_cfg=idle_cfg, stream_spec=ss,
+                outputs=out, flags=flags, stream_end=ns, step_begin=s0, step_end=min(steps, s0 + chunk))
+    if keep_on_device:
+        return BatchResult(agg, state, rec, od, table.candidates)
+    torch.cuda.synchronize(dev)
+    return BatchResult(
+        agg.cpu().numpy(), {k: v.cpu().numpy() for k, v in state.items()},
+        {k: v.cpu().numpy() for k, v in rec.items()}, None if od is None else od.cpu().numpy(),
+        table.candidates,
+    )
+
+
+class HostStreamer:
+    """run_batch for traces that live in (pinned) HOST memory.
+
+    The time-major slow-down array is cut into step chunks; chunk i+1 is
+    copied host->device on a copy stream while the kernel runs chunk i on the
+    compute stream (double buffer, CUDA events), with the filter state and
+    aggregates carried on the device between chunks (alert_run step ranges).
+    This is the end-to-end path: inputs from host, per-stream summaries back.
+    """
+
+    def __init__(self, space, specs, packed: PackedEnvs, policy: str = "alert", *, kalman=None,
+                 idle_cfg=None, group_sizes=None, stream_spec=None, chunk_steps: int = 1000,
+                 engine: Engine | None = None, device: int = 0):
+        torch = __import__("torch")
+        self.torch = torch
+        self.eng = eng = engine or get_engine(device)
+        self.table = eng.table(space)
+        self.specs = specs if isinstance(specs, np.ndarray) and specs.dtype == abi.SPEC_DTYPE \
+            else pack_specs(list(specs), group_sizes)
+        self.policy = policy_code(policy)
+        self.kalman, self.idle_cfg = kalman, idle_cfg
+        self.n_steps, self.n_streams = packed.slowdown.shape
+        self.chunk = min(chunk_steps, self.n_steps)
+        d = eng.tdev
+        # pinned host copy of the inputs (outside any timed region)
+        self.host = torch.from_numpy(np.ascontiguousarray(packed.slowdown)).pin_memory()
+        self.seg = [torch.from_numpy(a).to(d) for a in (packed.n_segments, packed.seg_end, packed.seg_phase,
+                                                        packed.seg_idle)]
+        self.ss = None if stream_spec is None else torch.as_tensor(np.asarray(stream_spec, np.int32)).to(d)
+        self.bufs = [torch.empty((self.chunk, self.n_streams), dtype=self.host.dtype, device=d) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(d)
+        self.agg_host = torch.empty((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64).pin_memory()
+
+    @property
+    def h2d_bytes(self) -> int:
+        return self.host.numel() * self.host.element_size()
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.agg_host.numel() * self.agg_host.element_size()
+
+    def run(self):
+        """One end-to-end pass; returns the pinned host aggregate tensor."""
+        torch, eng = self.torch, self.eng
+        comp = torch.cuda.current_stream(eng.tdev)
+        self.copy_stream.wait_stream(comp)  # copies are ordered after the caller's prior work
+        state = eng.new_state(self.table, self.n_streams, self.kalman, self.idle_cfg)
+        agg = torch.zeros((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64, device=eng.tdev)
+        out = outputs_struct(None, agg=agg)
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        consumed = [torch.cuda.Event(), torch.cuda.Event()]
+        starts = list(range(0, self.n_steps, self.chunk))
+
+        def issue_copy(i):
+            b = i % 2
+            s0 = starts[i]
+            s1 = min(self.n_steps, s0 + self.chunk)
+            with torch.cuda.stream(self.copy_stream):
+                if i >= 2:
+                    self.copy_stream.wait_event(consumed[b])
+                self.bufs[b][: s1 - s0].copy_(self.host[s0:s1], non_blocking=True)
+                copied[b].record(self.copy_stream)
+
+        issue_copy(0)
+        for i, s0 in enumerate(starts):
+            s1 = min(self.n_steps, s0 + self.chunk)
+            if i + 1 < len(starts):
+                issue_copy(i + 1)
+            b = i % 2
+            comp.wait_event(copied[b])
+            tr = DeviceTrace(self.bufs[b][: s1 - s0], *self.seg, stream_row=None, step_offset=s0)
+            eng.run(self.table, self.specs, tr, state, policy=self.policy, kalman=self.kalman,
+                    idle_cfg=self.idle_cfg, stream_spec=self.ss, outputs=out, stream_end=self.n_streams,
+                    step_begin=s0, step_end=s1)
+            consumed[b].record(comp)
+        self.agg_host.copy_(agg, non_blocking=True)
+        return self.agg_host
+
+
+def run(space, spec, trace, policy) -> RunResult:
+    """Drop-in for simulator.run (simulator.py:461-507) with a policy from
+    :func:`make_policy`: realize the trace (same numpy draws as the
+    reference), then one fused GPU launch over all inputs.  Records carry
+    FP64 values; ``decision.prediction`` is not materialised (None)."""
+    from .policies import GpuPolicy
+
+    if not isinstance(policy, GpuPolicy):
+        raise TypeError("run() executes the policies of paper_1911_00119_b200.make_policy on the GPU; "
+                        f"got {type(policy).__name__}")
+    env = realize(trace)
+    policy.begin(space, spec, env)
+    res = run_batch(space, [spec], [env], policy.code_name, kalman=policy.kalman,
+                    idle_cfg=getattr(policy, "idle_cfg", None), group_sizes=trace.group_size,
+                    records="f64", trace_dtype=np.float64, device=policy.device)
+    policy._finish(res)
+    d = res.decoded()
+    cands = res.candidates
+    recs = []
+    for n in range(len(env.slowdown)):
+        c = int(d["cand"][n, 0])
+        dec = decision_of(cands, c, int(d["level"][n, 0]))
+        recs.append(StepRecord(
+            input_index=n, decision=dec, true_slowdown=float(env.slowdown[n]),
+            observed_latency=float(res.records["latency"][n, 0]), completed_stage=int(d["completed"][n, 0]),
+            deadline_met=bool(d["met"][n, 0]), delivered_accuracy=float(res.records["accuracy"][n, 0]),
+            energy=float(res.records["energy"][n, 0]),
+            violations=ViolationFlags(bool(d["viol_lat"][n, 0]), bool(d["viol_acc"][n, 0]),
+                                      bool(d["viol_energy"][n, 0])),
+            phase_index=int(env.phase_index[n]), idle_power_true=float(env.idle_power[n]),
+        ))
+    return RunResult(tuple(recs), summary_from_agg(res.agg[0], len(trace.phases)))
+
+
+def run_injected(space, spec, env: TrueEnvironment, policy: str = "alert", *, kalman=None,
+                 group_size=None, forced=None, records: str = "f64", trace_dtype=np.float64,
+                 device: int = 0, flags: int = 0) -> BatchResult:
+    """One stream over an already-realized environment (parity harness)."""
+    f = None if forced is None else np.asarray(forced, np.int32).reshape(-1, 1)
+    return run_batch(space, [spec], [env], policy, kalman=kalman, group_sizes=group_size, records=records,
+                     forced=f, trace_dtype=trace_dtype, device=device, flags=flags)

@@ -125,3 +125,47 @@ def preset_phases(lengths=(200, 200, 200), input_noise_sd: float = 0.05, order=(
 
 def preset_trace(seed: int = 42, phase_length: int = 200, input_noise_sd: float = 0.05) -> Trace:
     return Trace(seed=seed, phases=preset_phases((phase_length,) * 3, input_noise_sd))
+
+
+def _realize_block(args):
+    from .trace import realize
+
+    seeds, lengths, noise, order, dtype = args
+    phases = preset_phases(lengths, noise, order)
+    out = np.empty((sum(lengths), len(seeds)), dtype=dtype)
+    for c, sd in enumerate(seeds):
+        out[:, c] = realize(Trace(seed=int(sd), phases=phases)).slowdown
+    return out
+
+
+def preset_batch(n_streams: int, lengths=(3334, 3333, 3333), seed0: int = 42, input_noise_sd: float = 0.05,
+                 order=(0, 1, 2), dtype=np.float32, processes: int | None = None):
+    """Realized preset-contention traces for streams k = 0..n-1 with seeds
+    seed0 + k (each column identical to realize(Trace(seed0 + k, ...))),
+    packed time-major for the device.  Realization is spread over host
+    processes; it is input preparation, not part of the timed hot path."""
+    import multiprocessing as mp
+    import os
+
+    from .trace import PackedEnvs
+
+    seeds = np.arange(seed0, seed0 + n_streams)
+    procs = processes or min(os.cpu_count() or 1, 64)
+    blocks = np.array_split(seeds, max(1, min(n_streams, procs * 4)))
+    jobs = [(b, tuple(lengths), input_noise_sd, tuple(order), dtype) for b in blocks if len(b)]
+    if procs > 1 and n_streams > 256:
+        with mp.get_context("fork").Pool(procs) as pool:
+            parts = pool.map(_realize_block, jobs)
+    else:
+        parts = [_realize_block(j) for j in jobs]
+    slow = np.concatenate(parts, axis=1)
+    regimes_idle = (4.0, 6.0, 5.0)
+    nseg = len(lengths)
+    ends = np.cumsum(lengths).astype(np.int32)
+    return PackedEnvs(
+        slowdown=slow,
+        n_segments=np.full(n_streams, nseg, np.int32),
+        seg_end=np.tile(ends, (n_streams, 1)),
+        seg_phase=np.tile(np.arange(nseg, dtype=np.int32), (n_streams, 1)),
+        seg_idle=np.tile(np.array([regimes_idle[r] for r in order], np.float64), (n_streams, 1)),
+    )
