@@ -222,7 +222,7 @@ def main():
     ap.add_argument("--streams", type=int, default=None, help="override streams per rank")
     ap.add_argument("--trace-steps", type=int, default=None, help="override steps per stream")
     ap.add_argument("--lanes", type=int, default=0)
-    ap.add_argument("--tpb", type=int, default=0)
+    ap.add_argument("--tpb", type=int, default=0)  # 0 = library default (64)
     ap.add_argument("--records", default="none", choices=["none", "f32"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

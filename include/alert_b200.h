@@ -282,6 +282,10 @@ int64_t alert_launch_count(AlertContext* ctx);
  * the FP32 roofline (instrumentation, not part of the scheduling path). */
 int alert_probe_fp32_peak(int device, double* slots_per_s);
 
+/* The scan's FP32 normal CDF: out[i] = Phi(sqrt(2) * x[i]) for device arrays
+ * (instrumentation: lets tests bound its error against FP64). */
+int alert_probe_phi32(const float* x, float* out, int64_t n, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

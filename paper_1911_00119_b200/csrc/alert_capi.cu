@@ -33,7 +33,7 @@ static int fail(int code, const std::string& msg) {
 struct AlertContext {
   int device = 0;
   int lanes = 0;  // 0 = auto
-  int tpb = 128;
+  int tpb = 64;
   int n_sm = 148;
   int max_smem = 227 * 1024;
   std::atomic<long long> launches{0};
@@ -64,6 +64,7 @@ __global__ void predict_kernel(const StepParams P, AlertPrediction* out, const i
     const AlertSpec spec = P.specs[si];
     StepCtx x;
     make_ctx(x, &spec, P.st.mu[i], P.st.sigma2[i], P.st.phi[i], P.goal[i], true);
+    ensure_fp64(x);
     Pred64 q = eval64(P.T, x, cell);
     AlertPrediction r;
     double t = P.T.t64[cell];
@@ -182,7 +183,7 @@ int alert_set_launch(AlertContext* ctx, int lanes, int tpb) {
   if (tpb != 0 && (tpb < 32 || tpb > 256 || tpb % 32))
     return fail(ALERT_ERR_INVALID_ARGUMENT, "threads_per_block must be a multiple of 32 in [32, 256]");
   ctx->lanes = lanes;
-  ctx->tpb = tpb ? tpb : 128;
+  ctx->tpb = tpb ? tpb : 64;
   return ALERT_OK;
 }
 
@@ -291,12 +292,12 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     double qf = d->dnn_q_fail[i];
     double prev = k0 == 0 ? qf : d->stage_accuracy[stage_off[i] + k0 - 1];
     uint32_t key = ((uint32_t)j << 20) | ((uint32_t)i << 8) | (uint32_t)st;
-    A[cell] = make_float4((float)(1.0 / t), (float)t, (float)d->power_cap[j], (float)(a - prev));
+    A[cell] = make_float4((float)(1.0 / t), (float)(d->power_cap[j] * t), (float)(a - prev), (float)qf);
     float kb, cb, sb;
     memcpy(&kb, &key, 4);
     memcpy(&cb, &cand, 4);
     memcpy(&sb, &st, 4);
-    B[cell] = make_float4((float)qf, kb, cb, sb);
+    B[cell] = make_float4((float)t, kb, cb, sb);
     t64[cell] = t;
     a64[cell] = a;
     qf64[cell] = qf;

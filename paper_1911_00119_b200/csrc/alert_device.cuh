@@ -41,8 +41,8 @@ struct DevTable {
   int n_trad;       // cells [0, n_trad) are traditional, one per (dnn, power)
   int n_any_cols;   // anytime columns (dnn, power) after the traditional cells
   int n_powers;
-  const float4* cellA;    // {1/t, t, cap, d = a_k - a_{k-1} (a_0 = q_fail)}
-  const float4* cellB;    // {q_fail, key bits, candidate index bits, stage bits}
+  const float4* cellA;    // {1/t, cap*t, d = a_k - a_{k-1} (a_0 = q_fail), q_fail}   FP32 scan
+  const float4* cellB;    // {t, tie-key bits, candidate index bits, stage bits}   refine / decode
   const int2* any_cols;   // {first cell, number of stages}
   const double* t64;      // profiled latency of the cell's stage at its power
   const double* a64;      // stage accuracy
@@ -71,9 +71,39 @@ __device__ __forceinline__ void neumaier(double& s, double& c, double x) {
   s = t;
 }
 
-// Standard normal CDF, FP32 (predictor.py:25-27 in single precision).
-__device__ __forceinline__ float phi32(float z) {
-  return fmaf(0.5f, erff(z * 0.70710678118654752f), 0.5f);
+// Standard normal CDF in FP32 from x = z / sqrt(2):
+//   erfc(a) = t * exp(-a^2 + P(t)),  t = 1 / (1 + a/2),  a = |x|
+// (rational-exponential form with a degree-9 polynomial; relative error
+// <= 1.2e-7 over a >= 0), Phi = 1 - erfc(a)/2 for x >= 0 else erfc(a)/2.
+// One branch-free formula: 1 FFMA + RCP + 9 FFMA (immediate coefficients) +
+// 2 FFMA + EX2 + FMUL + FADD/FSEL.  Absolute error bound used by the
+// near-tie logic: ALERT_PHI32_ERR (checked on the GPU, tests/test_gpu_parity.py).
+#define ALERT_PHI32_ERR_EPS 4.0f  // in units of 2^-23
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float phi32_x(float x) {
+  const float a = fabsf(x);
+  const float t = rcp_approx(fmaf(0.5f, a, 1.0f));
+  float p = fmaf(t, 0.17087277f, -0.82215223f);
+  p = fmaf(t, p, 1.48851587f);
+  p = fmaf(t, p, -1.13520398f);
+  p = fmaf(t, p, 0.27886807f);
+  p = fmaf(t, p, -0.18628806f);
+  p = fmaf(t, p, 0.09678418f);
+  p = fmaf(t, p, 0.37409196f);
+  p = fmaf(t, p, 1.00002368f);
+  p = fmaf(t, p, -1.26551223f);
+  const float arg = fmaf(-a, a, p);                                    // ln(erfc(a) / t)
+  const float h = t * ex2_approx(fmaf(arg, 1.44269504088896341f, -1.0f));  // erfc(a) / 2
+  return x >= 0.0f ? 1.0f - h : h;
 }
 
 // deadline_probability, exact reference arithmetic (predictor.py:48-65).
@@ -91,8 +121,9 @@ struct StepCtx {
   // FP64 state (exact path)
   double mu, sig, phi, goal, zq;
   const AlertSpec* spec;
-  // FP32 scan inputs
-  float goal_f, mu_f, inv_sig, mu_e, omp, phig;
+  // FP32 scan inputs: x = (goal/t - mu) * inv_sig_s  (= z / sqrt 2),
+  //                   E = (cap t) * max(mu_e, phig / t + ompmu)
+  float goal_f, mu_f, inv_sig_s, mu_e, ompmu, phig;
   // FP32 error bounds
   float d_pr, d_acc, d_erel;
   // thresholds with margins
@@ -100,31 +131,40 @@ struct StepCtx {
   bool fp64_all;
 };
 
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Per-step scan context.  Only FP32 work here: the FP64 sigma (sqrt) is
+// computed lazily by ensure_fp64() when the re-rank needs exact values.
 __device__ __forceinline__ void make_ctx(StepCtx& x, const AlertSpec* sp, double mu, double sigma2,
                                          double phi, double goal, bool fp64_all) {
   x.spec = sp;
   x.mu = mu;
-  x.sig = sqrt(sigma2);  // sigma2 ** 0.5 (estimator.py:42-44)
+  x.sig = sigma2;  // holds sigma2 until ensure_fp64()
   x.phi = phi;
   x.goal = goal;
   x.zq = sp->z_q;
   x.goal_f = (float)goal;
   x.mu_f = (float)mu;
-  float sig_f = (float)x.sig;
-  x.inv_sig = 1.0f / sig_f;
-  double mu_e = sp->has_pr ? xadd(mu, xmul(sp->z_q, x.sig)) : mu;  // predictor.py:140
-  x.mu_e = (float)mu_e;
-  float phi_f = (float)phi;
-  x.omp = 1.0f - phi_f;
+  const float s2f = (float)sigma2;
+  const float inv_sig = rsqrt_approx(s2f);  // MUFU.RSQ, rel. error <= 2 ulp
+  x.inv_sig_s = inv_sig * 0.70710678118654752f;
+  const float sig_f = s2f * inv_sig;
+  x.mu_e = sp->has_pr ? fmaf((float)sp->z_q, sig_f, x.mu_f) : x.mu_f;  // predictor.py:140
+  const float phi_f = (float)phi;
+  x.ompmu = (1.0f - phi_f) * x.mu_e;
   x.phig = phi_f * x.goal_f;
-  float r = fabsf(x.mu_f) * x.inv_sig;
-  // |dPhi| <= eps*(0.625 + 0.6*mu/sigma) from rounding of z, + erff / blend error,
-  // times a safety factor of 2.
-  x.d_pr = 2.0f * kEps * (0.625f + 0.6f * r + 2.0f);
+  const float r = fabsf(x.mu_f) * inv_sig;
+  // |dPhi| <= eps*(1.0 + 0.6*mu/sigma) from the rounding of z (incl. the
+  // approximate rsqrt), plus the Phi32 evaluation error, times 2 for safety.
+  x.d_pr = 2.0f * kEps * (1.0f + 0.6f * r + ALERT_PHI32_ERR_EPS);
   x.d_acc = x.d_pr + 8.0f * kEps;
   x.d_erel = 12.0f * kEps;
-  x.fp64_all = fp64_all || !(sig_f > 0.0f) || !isfinite(x.inv_sig) || !isfinite(x.d_pr) ||
-               !(fabs(mu_e) < 1e30);
+  x.fp64_all = fp64_all || !(s2f > 0.0f) || !isfinite(inv_sig) || !isfinite(x.d_pr) ||
+               !(fabsf(x.mu_e) < 1e30f) || !(x.mu_e >= 0.0f);
   x.q_hi = (float)sp->q_goal + x.d_acc;
   x.q_lo = (float)sp->q_goal - x.d_acc;
   x.th_hi = (float)sp->pr_threshold + x.d_pr;
@@ -132,6 +172,9 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const AlertSpec* sp, double
   x.e_hi = (float)sp->e_goal * (1.0f - x.d_erel);  // sure: E <= e_hi
   x.e_lo = (float)sp->e_goal * (1.0f + x.d_erel);  // possible: E <= e_lo
 }
+
+// sigma = sigma2 ** 0.5 (estimator.py:42-44) for the exact FP64 path.
+__device__ __forceinline__ void ensure_fp64(StepCtx& x) { x.sig = sqrt(x.sig); }
 
 // --------------------------------------------------------------------------
 // FP32 running top-2 per fallback level
@@ -193,8 +236,7 @@ struct Pred64 {
 
 __device__ __forceinline__ Pred64 eval64(const DevTable& T, const StepCtx& x, int c) {
   Pred64 r;
-  float4 B = T.cellB[c];
-  int stage = __float_as_int(B.w);  // 0 = traditional
+  const int stage = __float_as_int(T.cellB[c].w);  // 0 = traditional
   double t = T.t64[c];
   double qf = T.qf64[c];
   r.pr = phi64(x.goal, x.mu, x.sig, t);
@@ -259,6 +301,11 @@ __device__ __forceinline__ bool energy_objective(int level) {
   return MODE == ALERT_MODE_MIN_ENERGY && level == 0;
 }
 
+// Which fallback levels a pass tracks: the FP32 scan tracks the constrained
+// levels (0, and 1 for max-accuracy); level 2 (no constraints, max accuracy)
+// is scanned only when those are empty (rare), saving its tracker per cell.
+enum { TRACK_CONSTRAINED = 0, TRACK_L2 = 1 };
+
 template <int MODE, bool HAS_PR>
 struct AlertScan {
   Tracker t[3];
@@ -283,7 +330,12 @@ struct AlertScan {
     v = energy_objective<MODE>(lvl) ? E : -acc;
   }
 
+  template <int TRACK>
   __device__ __forceinline__ void scan_cell(const StepCtx& x, int c, float pr, float acc, float E) {
+    if (TRACK == TRACK_L2) {
+      t[2].push(-acc, true, false, c);
+      return;
+    }
     bool s, p;
     float v;
     classify(x, 0, pr, acc, E, s, p, v);
@@ -292,7 +344,6 @@ struct AlertScan {
       classify(x, 1, pr, acc, E, s, p, v);
       t[1].push(v, s, p && !s, c);
     }
-    if (MODE == ALERT_MODE_MIN_ENERGY || HAS_PR) t[2].push(-acc, true, false, c);
   }
 
   __device__ __forceinline__ void refine_cell(const DevTable& T, const StepCtx& x, int c, float pr,
@@ -319,8 +370,17 @@ __device__ __forceinline__ float cutoff(const StepCtx& x, int level, float b1) {
   return b1 + 2.0f * x.d_acc;
 }
 
+// FP32 prediction of one cell: pr, expected accuracy (running along an
+// anytime column: acc_k = acc_{k-1} + Phi_k * (a_k - a_{k-1})), energy.
+__device__ __forceinline__ void predict32(const StepCtx& x, const float4& A, float base, float& pr,
+                                          float& acc, float& E) {
+  pr = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
+  acc = fmaf(pr, A.z, base);
+  E = A.y * fmaxf(x.mu_e, fmaf(x.phig, A.x, x.ompmu));
+}
+
 // One pass over the cells (PASS 0 = FP32 scan, 1 = refine at scan.level).
-template <int PASS, int MODE, bool HAS_PR, class Tile>
+template <int PASS, int TRACK, int MODE, bool HAS_PR, class Tile>
 __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __restrict__ sA,
                                           const float4* __restrict__ sB, const int2* __restrict__ sCol,
                                           const Tile& tile, const StepCtx& x, int kinds,
@@ -329,35 +389,25 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
   const int lane = tile.thread_rank();
   const bool skip32 = PASS == 1 && S.all;
   if (kinds & 1) {
+#pragma unroll 4
     for (int c = lane; c < T.n_trad; c += W) {
-      float4 A = sA[c];
+      const float4 A = sA[c];
       float pr = 0.f, acc = 0.f, E = 0.f;
-      if (!skip32) {
-        float qf = sB[c].x;
-        pr = phi32(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig);
-        acc = fmaf(pr, A.w, qf);
-        float lat = x.mu_e * A.y;
-        E = A.z * fmaxf(lat, fmaf(x.omp, lat, x.phig));
-      }
-      if (PASS == 0) S.scan_cell(x, c, pr, acc, E);
+      if (!skip32) predict32(x, A, A.w, pr, acc, E);
+      if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
       else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
     }
   }
   if (kinds & 2) {
     for (int col = lane; col < T.n_any_cols; col += W) {
-      int2 cd = sCol[col];
-      float acc = sB[cd.x].x;
+      const int2 cd = sCol[col];
+      float acc = sA[cd.x].w;
       for (int k = 0; k < cd.y; ++k) {
-        int c = cd.x + k;
-        float4 A = sA[c];
+        const int c = cd.x + k;
+        const float4 A = sA[c];
         float pr = 0.f, E = 0.f;
-        if (!skip32) {
-          pr = phi32(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig);
-          acc = fmaf(pr, A.w, acc);
-          float lat = x.mu_e * A.y;
-          E = A.z * fmaxf(lat, fmaf(x.omp, lat, x.phig));
-        }
-        if (PASS == 0) S.scan_cell(x, c, pr, acc, E);
+        if (!skip32) predict32(x, A, acc, pr, acc, E);
+        if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
         else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
       }
     }
@@ -367,7 +417,7 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
 // AlertPolicy.decide (policies.py:97-103) for the tile's stream.
 template <int MODE, bool HAS_PR, class Tile>
 __device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const float4* sB,
-                                   const int2* sCol, const Tile& tile, const StepCtx& x, int kinds,
+                                   const int2* sCol, const Tile& tile, StepCtx& x, int kinds,
                                    bool no_refine) {
   AlertScan<MODE, HAS_PR> S;
 #pragma unroll
@@ -378,9 +428,16 @@ __device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const fl
   Decision d{-1, 0, false};
   int start = 0;
   if (!x.fp64_all) {
-    cell_pass<0>(T, sA, sB, sCol, tile, x, kinds, S);
-#pragma unroll
-    for (int l = 0; l < 3; ++l) S.t[l].merge(tile);
+    cell_pass<0, TRACK_CONSTRAINED>(T, sA, sB, sCol, tile, x, kinds, S);
+    S.t[0].merge(tile);
+    if (MODE == ALERT_MODE_MAX_ACCURACY) S.t[1].merge(tile);
+    // level 2 is needed only if every constrained level is empty (uniform per tile)
+    const bool need_l2 = !(S.t[0].b1 < kInfF) && !(S.t[0].un < kInfF) &&
+                         (MODE == ALERT_MODE_MIN_ENERGY || (HAS_PR && !(S.t[1].b1 < kInfF) && !(S.t[1].un < kInfF)));
+    if ((MODE == ALERT_MODE_MIN_ENERGY || HAS_PR) && need_l2) {
+      cell_pass<0, TRACK_L2>(T, sA, sB, sCol, tile, x, kinds, S);
+      S.t[2].merge(tile);
+    }
     start = -1;
     bool done = false;
 #pragma unroll
@@ -406,19 +463,21 @@ __device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const fl
         const int L = (li == 1 && MODE == ALERT_MODE_MIN_ENERGY) ? 2 : li;
         if (li >= start && d.cell < 0 && S.t[L].b1 < kInfF) { d.cell = S.t[L].i1; d.level = L; }
       }
-      return d;
+      if (d.cell >= 0) return d;
     }
   }
-  // FP64 re-rank, level by level from the first uncertain one
+  // FP64 re-rank, level by level from the first uncertain one.  A level-2
+  // tracker that was never scanned keeps b1 = inf: every candidate is relevant.
+  ensure_fp64(x);
 #pragma unroll
   for (int li = 0; li < NL; ++li) {
     const int L = (li == 1 && MODE == ALERT_MODE_MIN_ENERGY) ? 2 : li;
     if (li >= start && d.cell < 0) {
       S.level = L;
-      S.all = x.fp64_all;
-      S.cut = x.fp64_all ? kInfF : cutoff<MODE>(x, L, S.t[L].b1);
+      S.all = x.fp64_all || (L == 2 && !(S.t[2].b1 < kInfF));  // level 2 never scanned: all relevant
+      S.cut = S.all ? kInfF : cutoff<MODE>(x, L, S.t[L].b1);
       S.best.init();
-      cell_pass<1>(T, sA, sB, sCol, tile, x, kinds, S);
+      cell_pass<1, TRACK_CONSTRAINED>(T, sA, sB, sCol, tile, x, kinds, S);
       S.best.merge(tile);
       if (S.best.cell >= 0) {
         d.cell = S.best.cell;
@@ -432,7 +491,7 @@ __device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const fl
 
 template <class Tile>
 __device__ __forceinline__ Decision alert_decide(const DevTable& T, const float4* sA, const float4* sB,
-                                                 const int2* sCol, const Tile& tile, const StepCtx& x,
+                                                 const int2* sCol, const Tile& tile, StepCtx& x,
                                                  int kinds, bool no_refine) {
   if (x.spec->mode == ALERT_MODE_MIN_ENERGY) {
     if (x.spec->has_pr) return alert_decide_t<ALERT_MODE_MIN_ENERGY, true>(T, sA, sB, sCol, tile, x, kinds, no_refine);

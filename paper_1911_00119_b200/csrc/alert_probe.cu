@@ -49,3 +49,19 @@ int alert_probe_fp32_peak(int device, double* slots_per_s) {
   *slots_per_s = (double)blocks * threads * iters * 16.0 * 8.0 / (best * 1e-3);
   return ALERT_OK;
 }
+
+#include "alert_device.cuh"
+
+__global__ void phi32_probe_kernel(const float* x, float* out, long long n) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = alert::phi32_x(x[i]);
+}
+
+// The FP32 normal CDF of the scan, Phi(sqrt(2) * x[i]) -> out[i] (device
+// pointers): lets the tests bound its error against FP64 (instrumentation).
+int alert_probe_phi32(const float* x, float* out, int64_t n, void* cuda_stream) {
+  if (!x || !out || n < 0) return ALERT_ERR_INVALID_ARGUMENT;
+  if (n == 0) return ALERT_OK;
+  phi32_probe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)cuda_stream>>>(x, out, n);
+  return cudaGetLastError() == cudaSuccess ? ALERT_OK : ALERT_ERR_CUDA;
+}
