@@ -273,7 +273,8 @@ def main():
     import paper_1911_00119_b200 as A
     from paper_1911_00119_b200 import abi
     from paper_1911_00119_b200._lib import load
-    from paper_1911_00119_b200.engine import DeviceTrace, outputs_struct
+    from paper_1911_00119_b200.dist import max_over_ranks, reduce_aggregates
+    from paper_1911_00119_b200.engine import outputs_struct
     from paper_1911_00119_b200.packing import policy_code
     from paper_1911_00119_b200.simulator import HostStreamer
 
@@ -330,23 +331,13 @@ def main():
     ms = e0.elapsed_time(e1)
     gpu_launches = eng.launch_count() - launches0
     kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, dev)
     decisions = args.steps * S * N * world
     value = decisions / (ms * 1e-3)
 
     # final aggregate of the last step: deterministic per-GPU reduce, then the
     # one cross-GPU exchange (NCCL all_gather, summed in rank order)
-    total = eng.reduce(agg)
-    if world > 1:
-        parts = [torch.empty_like(total) for _ in range(world)]
-        dist.all_gather(parts, total)
-        total = parts[0].clone()
-        for p in parts[1:]:
-            total += p
-    tot = total.cpu().numpy()
+    tot = reduce_aggregates(eng.reduce(agg)).cpu().numpy()
     n_all = tot[abi.AGG_N]
     quality = {
         "mean_energy_j": float((tot[abi.AGG_ENERGY] + tot[abi.AGG_ENERGY_C]) / n_all),
@@ -416,10 +407,7 @@ def main():
             b.record(stream)
             torch.cuda.synchronize(dev)
             ems = a.elapsed_time(b)
-            if world > 1:
-                t = torch.tensor([ems], dtype=torch.float64, device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ems = float(t.item())
+            ems = max_over_ranks(ems, dev)
             e2e = {"value": decisions / (ems * 1e-3), "unit": "decisions/s",
                    "h2d_bytes_per_step": hs.h2d_bytes, "d2h_bytes_per_step": hs.d2h_bytes,
                    "path": "paper_1911_00119_b200.simulator.HostStreamer (pinned host trace, chunked H2D "

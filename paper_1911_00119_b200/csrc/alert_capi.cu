@@ -61,13 +61,12 @@ __global__ void predict_kernel(const StepParams P, AlertPrediction* out, const i
     const int c = (int)(g % P.T.n_cells);  // candidate index
     const int cell = P.T.cell_of_cand[c];
     const int si = P.stream_spec ? P.stream_spec[i] : (int)(i % P.n_specs);
-    const AlertSpec spec = P.specs[si];
     StepCtx x;
-    make_ctx(x, &spec, P.st.mu[i], P.st.sigma2[i], P.st.phi[i], P.goal[i], true);
+    make_ctx(x, P.specs + si, P.T.c64, P.st.mu[i], P.st.sigma2[i], P.st.phi[i], P.goal[i], true);
     ensure_fp64(x);
     Pred64 q = eval64(P.T, x, cell);
     AlertPrediction r;
-    double t = P.T.t64[cell];
+    double t = P.T.c64[cell].t;
     r.latency_mean = xmul(x.mu, t);
     r.latency_sigma = xmul(x.sig, t);
     r.pr_deadline = q.pr;
@@ -86,8 +85,10 @@ __global__ void observe_kernel(const DevTable T, const AlertFilterConfig cfg, Al
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   Filter f{st.mu[i], st.sigma2[i], st.k_gain[i], st.q_noise[i], st.innov[i], st.phi[i], st.m_var[i]};
-  slowdown_update(cfg, f, fb_lat[i], fb_t[i]);
-  idle_update(cfg, f, idle[i], T.power_cap64[power[i]]);
+  bool k_valid = false;
+  int ik = -1;
+  slowdown_update(cfg, f, fb_lat[i], fb_t[i], k_valid);
+  idle_update(cfg, f, py_min(1.0, xdiv(idle[i], T.power_cap64[power[i]])), ik, -1, nullptr, nullptr);
   st.mu[i] = f.mu; st.sigma2[i] = f.sigma2; st.k_gain[i] = f.k_gain; st.q_noise[i] = f.q_noise;
   st.innov[i] = f.innov; st.phi[i] = f.phi; st.m_var[i] = f.m_var;
 }
@@ -280,7 +281,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     q += ns;
   }
   std::vector<float4> A(n), B(n);
-  std::vector<double> t64(n), a64(n), qf64(n), cap64(n);
+  std::vector<Cell64> c64(n);
   std::vector<int> cell_of_cand(n);
   double max_cap = d->power_cap[P - 1];
   for (int cell = 0; cell < n; ++cell) {
@@ -298,16 +299,13 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     memcpy(&cb, &cand, 4);
     memcpy(&sb, &st, 4);
     B[cell] = make_float4((float)t, kb, cb, sb);
-    t64[cell] = t;
-    a64[cell] = a;
-    qf64[cell] = qf;
-    cap64[cell] = d->power_cap[j];
+    c64[cell] = Cell64{t, a, qf, d->power_cap[j]};
     cell_of_cand[cand] = cell;
   }
   size_t bytes = 0;
   auto place = [&](size_t sz) { size_t o = (bytes + 255) & ~size_t(255); bytes = o + sz; return o; };
   size_t oA = place(sizeof(float4) * n), oB = place(sizeof(float4) * n), oC = place(sizeof(int2) * (cols.size() + 1));
-  size_t oT = place(8 * n), oAcc = place(8 * n), oQ = place(8 * n), oCap = place(8 * n), oCell = place(4 * n);
+  size_t oC64 = place(sizeof(Cell64) * n), oCell = place(4 * n);
   size_t oPw = place(8 * P);
   CUDA_TRY(cudaSetDevice(ctx->device));
   char* buf = nullptr;
@@ -320,10 +318,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   memcpy(&h[oA], A.data(), sizeof(float4) * n);
   memcpy(&h[oB], B.data(), sizeof(float4) * n);
   if (!cols.empty()) memcpy(&h[oC], cols.data(), sizeof(int2) * cols.size());
-  memcpy(&h[oT], t64.data(), 8 * n);
-  memcpy(&h[oAcc], a64.data(), 8 * n);
-  memcpy(&h[oQ], qf64.data(), 8 * n);
-  memcpy(&h[oCap], cap64.data(), 8 * n);
+  memcpy(&h[oC64], c64.data(), sizeof(Cell64) * n);
   memcpy(&h[oCell], cell_of_cand.data(), 4 * n);
   memcpy(&h[oPw], d->power_cap, 8 * P);
   e = cudaMemcpy(buf, h.data(), bytes, cudaMemcpyHostToDevice);
@@ -340,10 +335,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   T.cellA = reinterpret_cast<const float4*>(buf + oA);
   T.cellB = reinterpret_cast<const float4*>(buf + oB);
   T.any_cols = reinterpret_cast<const int2*>(buf + oC);
-  T.t64 = reinterpret_cast<const double*>(buf + oT);
-  T.a64 = reinterpret_cast<const double*>(buf + oAcc);
-  T.qf64 = reinterpret_cast<const double*>(buf + oQ);
-  T.cap64 = reinterpret_cast<const double*>(buf + oCap);
+  T.c64 = reinterpret_cast<const Cell64*>(buf + oC64);
   T.cell_of_cand = reinterpret_cast<const int*>(buf + oCell);
   double r = d->p_idle_prof / max_cap;
   T.phi0 = (1.0 < r) ? 1.0 : r;  // min(1.0, p_idle_prof / max cap), policies.py:90
@@ -407,9 +399,21 @@ static size_t table_smem(const AlertTable* tb) {
   return sizeof(float4) * 2 * (size_t)tb->dev.n_cells + sizeof(int2) * (size_t)(tb->dev.n_any_cols + 1);
 }
 
-static size_t run_smem(const AlertTable* tb, int tpb, int W) {
-  size_t base = (table_smem(tb) + 15) & ~size_t(15);
-  return base + sizeof(TileAgg) * (size_t)(tpb / W);
+// Staging decisions of run_kernel: specs, FP64 cells and the per-segment
+// idle-ratio table go to shared memory when small (see SmemLayout).
+static void run_staging(const AlertTable* tb, int n_specs, int tpb, int W, RunParams& P) {
+  const DevTable& T = tb->dev;
+  P.spec_smem = n_specs <= kSpecSmemMax;
+  P.c64_smem = T.n_cells <= kC64SmemMax;
+  P.ratio_smem = T.n_powers <= kRatioSmemMax &&
+                 (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;
+}
+
+static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const RunParams& P) {
+  const DevTable& T = tb->dev;
+  SmemLayout L(T.n_cells, T.n_any_cols, P.spec_smem ? n_specs : 0, P.c64_smem ? T.n_cells : 0, tpb / W,
+               P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg));
+  return L.total;
 }
 
 static int pick_lanes(const AlertContext* ctx, const AlertTable* tb) {
@@ -418,10 +422,60 @@ static int pick_lanes(const AlertContext* ctx, const AlertTable* tb) {
 }
 
 // Upload host specs to stream-ordered device memory (freed after the launch).
-static int upload_specs(const AlertSpec* specs, int n, cudaStream_t st, AlertSpec** dev) {
-  CUDA_TRY(cudaMallocAsync((void**)dev, sizeof(AlertSpec) * n, st));
-  CUDA_TRY(cudaMemcpyAsync(*dev, specs, sizeof(AlertSpec) * n, cudaMemcpyHostToDevice, st));
+// AlertSpec -> SpecDev (device form): goal0 / period0 with the reference's
+// operations (selector.py:48-70: max(t_goal - overhead, 0.001); simulator.py:483),
+// FP32 copies for the scan.
+static SpecDev spec_dev(const AlertSpec& a) {
+  SpecDev d{};
+  d.t_goal = a.t_goal;
+  d.e_goal = a.e_goal;
+  d.q_goal = a.q_goal;
+  d.pr_th = a.pr_threshold;
+  d.zq = a.z_q;
+  d.oh = a.overhead_budget;
+  volatile double g = a.t_goal - a.overhead_budget;  // no contraction / reassociation
+  double goal = (0.001 > g) ? 0.001 : (double)g;
+  d.goal0 = goal;
+  d.period0 = goal + a.overhead_budget;
+  d.q_f = (float)a.q_goal;
+  d.e_f = (float)a.e_goal;
+  d.th_f = (float)a.pr_threshold;
+  d.zq_f = (float)a.z_q;
+  d.mode = a.mode;
+  d.has_pr = a.has_pr;
+  d.group_size = a.group_size;
+  return d;
+}
+
+// Upload host specs to stream-ordered device memory (freed after the launch).
+static int upload_specs(const AlertSpec* specs, int n, cudaStream_t st, SpecDev** dev) {
+  std::vector<SpecDev> h(n);
+  for (int k = 0; k < n; ++k) h[k] = spec_dev(specs[k]);
+  CUDA_TRY(cudaMallocAsync((void**)dev, sizeof(SpecDev) * n, st));
+  CUDA_TRY(cudaMemcpyAsync(*dev, h.data(), sizeof(SpecDev) * n, cudaMemcpyHostToDevice, st));
+  // pageable source: the copy is staged before cudaMemcpyAsync returns
   return ALERT_OK;
+}
+
+// Idle-filter gain table (see RunParams): M_0 = m0, W_k = (M_k+s)/(M_k+s+v),
+// M_{k+1} = (1-W_k)(M_k+s), until M_{k+1} == M_k exactly.
+static void idle_table(const AlertFilterConfig& c, RunParams& P) {
+  P.idle_fix = -1;
+  volatile double m = c.m0;
+  for (int k = 0; k + 1 < kIdleTab; ++k) {
+    volatile double ms = m + c.s;
+    volatile double den = ms + c.v;
+    volatile double w = ms / den;
+    volatile double omw = 1.0 - w;
+    volatile double mn = omw * ms;
+    P.idle_m[k] = m;
+    P.idle_w[k] = w;
+    if (mn == m) {
+      P.idle_fix = k;
+      return;
+    }
+    m = mn;
+  }
 }
 
 static int dispatch_run(int W, int pf, const RunParams& P, int tpb, size_t smem, cudaStream_t st) {
@@ -484,14 +538,16 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
     return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: per-step outputs need strides");
   if (stream_end == stream_begin || step_end == step_begin) return ALERT_OK;
   int W = pick_lanes(ctx, tb);
-  size_t smem = run_smem(tb, ctx->tpb, W);
+  RunParams P;
+  run_staging(tb, n_specs, ctx->tpb, W, P);
+  size_t smem = run_smem(tb, n_specs, ctx->tpb, W, P);
   if ((int)smem > ctx->max_smem) return fail(ALERT_ERR_UNSUPPORTED, "alert_run: table exceeds shared memory");
+  idle_table(*cfg, P);
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  AlertSpec* dspecs = nullptr;
+  SpecDev* dspecs = nullptr;
   r = upload_specs(specs, n_specs, s, &dspecs);
   if (r) return r;
-  RunParams P;
   P.T = tb->dev;
   P.cfg = *cfg;
   P.specs = dspecs;
@@ -530,7 +586,7 @@ int alert_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs
   if ((int)smem > ctx->max_smem) return fail(ALERT_ERR_UNSUPPORTED, "alert_decide: table exceeds shared memory");
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  AlertSpec* dspecs = nullptr;
+  SpecDev* dspecs = nullptr;
   r = upload_specs(specs, n_specs, s, &dspecs);
   if (r) return r;
   StepParams P{};
@@ -569,7 +625,7 @@ int alert_predict(AlertContext* ctx, const AlertTable* tb, const AlertSpec* spec
   if (n <= 0) return n < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_predict: n < 0") : ALERT_OK;
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  AlertSpec* dspecs = nullptr;
+  SpecDev* dspecs = nullptr;
   r = upload_specs(specs, n_specs, s, &dspecs);
   if (r) return r;
   // per-candidate (dnn, power, stage) arrays in stream-ordered scratch
@@ -623,7 +679,7 @@ int alert_oracle_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec
   if (n <= 0) return n < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_oracle_decide: n < 0") : ALERT_OK;
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
-  AlertSpec* dspecs = nullptr;
+  SpecDev* dspecs = nullptr;
   r = upload_specs(specs, n_specs, s, &dspecs);
   if (r) return r;
   int W = pick_lanes(ctx, tb);

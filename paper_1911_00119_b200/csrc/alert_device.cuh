@@ -44,13 +44,26 @@ struct DevTable {
   const float4* cellA;    // {1/t, cap*t, d = a_k - a_{k-1} (a_0 = q_fail), q_fail}   FP32 scan
   const float4* cellB;    // {t, tie-key bits, candidate index bits, stage bits}   refine / decode
   const int2* any_cols;   // {first cell, number of stages}
-  const double* t64;      // profiled latency of the cell's stage at its power
-  const double* a64;      // stage accuracy
-  const double* qf64;     // q_fail of the cell's dnn
-  const double* cap64;    // power cap of the cell's power setting
+  const struct Cell64* c64;  // FP64 cell data (exact path), AoS
   const int* cell_of_cand;
   const double* power_cap64;  // [n_powers] caps by power index
   double phi0;            // min(1, p_idle_prof / max cap), policies.py:90
+};
+
+// FP64 data of one cell for the exact path: profiled latency of the cell's
+// stage at its power, stage accuracy, q_fail of its DNN, cap of its power.
+struct Cell64 {
+  double t, a, qf, cap;
+};
+
+// Device form of one AlertSpec, built on the host: the FP64 fields of the
+// reference spec, the per-stream constants of the step loop (goal and period
+// without groups, selector.py:48-70 / simulator.py:479-483, computed with the
+// reference's operations), and FP32 copies for the scan.
+struct SpecDev {
+  double t_goal, e_goal, q_goal, pr_th, zq, oh, goal0, period0;
+  float q_f, e_f, th_f, zq_f;
+  int mode, has_pr, group_size, pad;
 };
 
 // Exact FP64 helpers: no FMA contraction, Python's min/max semantics.
@@ -120,7 +133,8 @@ __device__ __forceinline__ double phi64(double goal, double mu, double sig, doub
 struct StepCtx {
   // FP64 state (exact path)
   double mu, sig, phi, goal, zq;
-  const AlertSpec* spec;
+  const SpecDev* spec;
+  const Cell64* c64;  // FP64 cell data (shared memory when it fits)
   // FP32 scan inputs: x = (goal/t - mu) * inv_sig_s  (= z / sqrt 2),
   //                   E = (cap t) * max(mu_e, phig / t + ompmu)
   float goal_f, mu_f, inv_sig_s, mu_e, ompmu, phig;
@@ -139,21 +153,22 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 
 // Per-step scan context.  Only FP32 work here: the FP64 sigma (sqrt) is
 // computed lazily by ensure_fp64() when the re-rank needs exact values.
-__device__ __forceinline__ void make_ctx(StepCtx& x, const AlertSpec* sp, double mu, double sigma2,
-                                         double phi, double goal, bool fp64_all) {
+__device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Cell64* c64, double mu,
+                                         double sigma2, double phi, double goal, bool fp64_all) {
   x.spec = sp;
+  x.c64 = c64;
   x.mu = mu;
   x.sig = sigma2;  // holds sigma2 until ensure_fp64()
   x.phi = phi;
   x.goal = goal;
-  x.zq = sp->z_q;
+  x.zq = sp->zq;
   x.goal_f = (float)goal;
   x.mu_f = (float)mu;
   const float s2f = (float)sigma2;
   const float inv_sig = rsqrt_approx(s2f);  // MUFU.RSQ, rel. error <= 2 ulp
   x.inv_sig_s = inv_sig * 0.70710678118654752f;
   const float sig_f = s2f * inv_sig;
-  x.mu_e = sp->has_pr ? fmaf((float)sp->z_q, sig_f, x.mu_f) : x.mu_f;  // predictor.py:140
+  x.mu_e = sp->has_pr ? fmaf(sp->zq_f, sig_f, x.mu_f) : x.mu_f;  // predictor.py:140
   const float phi_f = (float)phi;
   x.ompmu = (1.0f - phi_f) * x.mu_e;
   x.phig = phi_f * x.goal_f;
@@ -165,12 +180,12 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const AlertSpec* sp, double
   x.d_erel = 12.0f * kEps;
   x.fp64_all = fp64_all || !(s2f > 0.0f) || !isfinite(inv_sig) || !isfinite(x.d_pr) ||
                !(fabsf(x.mu_e) < 1e30f) || !(x.mu_e >= 0.0f);
-  x.q_hi = (float)sp->q_goal + x.d_acc;
-  x.q_lo = (float)sp->q_goal - x.d_acc;
-  x.th_hi = (float)sp->pr_threshold + x.d_pr;
-  x.th_lo = (float)sp->pr_threshold - x.d_pr;
-  x.e_hi = (float)sp->e_goal * (1.0f - x.d_erel);  // sure: E <= e_hi
-  x.e_lo = (float)sp->e_goal * (1.0f + x.d_erel);  // possible: E <= e_lo
+  x.q_hi = sp->q_f + x.d_acc;
+  x.q_lo = sp->q_f - x.d_acc;
+  x.th_hi = sp->th_f + x.d_pr;
+  x.th_lo = sp->th_f - x.d_pr;
+  x.e_hi = sp->e_f * (1.0f - x.d_erel);  // sure: E <= e_hi
+  x.e_lo = sp->e_f * (1.0f + x.d_erel);  // possible: E <= e_lo
 }
 
 // sigma = sigma2 ** 0.5 (estimator.py:42-44) for the exact FP64 path.
@@ -237,27 +252,28 @@ struct Pred64 {
 __device__ __forceinline__ Pred64 eval64(const DevTable& T, const StepCtx& x, int c) {
   Pred64 r;
   const int stage = __float_as_int(T.cellB[c].w);  // 0 = traditional
-  double t = T.t64[c];
-  double qf = T.qf64[c];
+  const Cell64* C = x.c64;
+  double t = C[c].t;
+  double qf = C[c].qf;
   r.pr = phi64(x.goal, x.mu, x.sig, t);
   if (stage == 0) {
-    r.acc = xadd(xmul(r.pr, T.a64[c]), xmul(xsub(1.0, r.pr), qf));  // accuracy_blend
+    r.acc = xadd(xmul(r.pr, C[c].a), xmul(xsub(1.0, r.pr), qf));  // accuracy_blend
   } else {
     // expected_accuracy_anytime (predictor.py:100-108), reference order,
     // streaming prs[m], prs[m+1] instead of materialising the list
     int first = c - (stage - 1);
-    double p_cur = stage == 1 ? r.pr : phi64(x.goal, x.mu, x.sig, T.t64[first]);
+    double p_cur = stage == 1 ? r.pr : phi64(x.goal, x.mu, x.sig, C[first].t);
     double acc = xmul(xsub(1.0, p_cur), qf);
     for (int m = 0; m < stage; ++m) {
       double p_next = (m + 1 == stage) ? 0.0
                       : (m + 2 == stage) ? r.pr
-                                         : phi64(x.goal, x.mu, x.sig, T.t64[first + m + 1]);
-      acc = xadd(acc, xmul(T.a64[first + m], xsub(p_cur, p_next)));
+                                         : phi64(x.goal, x.mu, x.sig, C[first + m + 1].t);
+      acc = xadd(acc, xmul(C[first + m].a, xsub(p_cur, p_next)));
       p_cur = p_next;
     }
     r.acc = acc;
   }
-  double p = T.cap64[c];
+  double p = C[c].cap;
   if (x.spec->has_pr) {  // predict_energy_percentile, predictor.py:129-144
     double lat = xmul(xadd(x.mu, xmul(x.zq, x.sig)), t);
     double idle = py_max(0.0, xsub(x.goal, py_min(lat, x.goal)));
@@ -271,8 +287,8 @@ __device__ __forceinline__ Pred64 eval64(const DevTable& T, const StepCtx& x, in
 
 // feasibility at a fallback level (selector.py:73-84, _LEVELS :94-99)
 __device__ __forceinline__ bool feasible64(const StepCtx& x, const Pred64& p, int level) {
-  const AlertSpec* s = x.spec;
-  if (level < 2 && s->has_pr && p.pr < s->pr_threshold) return false;
+  const SpecDev* s = x.spec;
+  if (level < 2 && s->has_pr && p.pr < s->pr_th) return false;
   if (s->mode == ALERT_MODE_MAX_ACCURACY) return level != 0 || p.energy <= s->e_goal;
   return level == 2 || p.acc >= s->q_goal;
 }
@@ -388,28 +404,53 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
   const int W = Tile::num_threads();
   const int lane = tile.thread_rank();
   const bool skip32 = PASS == 1 && S.all;
-  if (kinds & 1) {
-#pragma unroll 4
-    for (int c = lane; c < T.n_trad; c += W) {
-      const float4 A = sA[c];
-      float pr = 0.f, acc = 0.f, E = 0.f;
-      if (!skip32) predict32(x, A, A.w, pr, acc, E);
-      if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
-      else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
+  // Traditional cells: U cells per iteration, their table rows loaded one
+  // iteration ahead (register double buffer) so the shared-memory latency is
+  // off the critical path.  Indices are clamped for the look-ahead loads;
+  // out-of-range slots are not processed.
+  const int n = T.n_trad;
+  if ((kinds & 1) && n > 0) {
+    constexpr int U = 4;
+    float4 cur[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = sA[min(lane + u * W, n - 1)];
+    for (int c0 = lane; c0 < n; c0 += U * W) {
+      float4 nxt[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) nxt[u] = sA[min(c0 + (U + u) * W, n - 1)];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * W;
+        if (c < n) {
+          float pr = 0.f, acc = 0.f, E = 0.f;
+          if (!skip32) predict32(x, cur[u], cur[u].w, pr, acc, E);
+          if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
+          else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
     }
   }
-  if (kinds & 2) {
-    for (int col = lane; col < T.n_any_cols; col += W) {
-      const int2 cd = sCol[col];
-      float acc = sA[cd.x].w;
+  // Anytime columns: consecutive stages; the next stage row and the next
+  // column descriptor are prefetched one step ahead.
+  const int ncol = T.n_any_cols;
+  if ((kinds & 2) && lane < ncol) {
+    int2 cd = sCol[lane];
+    for (int col = lane; col < ncol; col += W) {
+      const int2 cd_next = sCol[min(col + W, ncol - 1)];
+      float4 A = sA[cd.x];
+      float acc = A.w;
       for (int k = 0; k < cd.y; ++k) {
         const int c = cd.x + k;
-        const float4 A = sA[c];
+        const float4 A_next = sA[cd.x + min(k + 1, cd.y - 1)];
         float pr = 0.f, E = 0.f;
         if (!skip32) predict32(x, A, acc, pr, acc, E);
         if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
         else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
+        A = A_next;
       }
+      cd = cd_next;
     }
   }
 }
@@ -512,42 +553,37 @@ struct Outcome {
   bool met, vl, va, ve;
 };
 
-__device__ __forceinline__ Outcome execute_measure(const DevTable& T, const AlertSpec* sp, int c, double s,
-                                                   double goal, double period, double idle) {
+__device__ __forceinline__ Outcome execute_measure(const float4* sB, const Cell64* C, const SpecDev* sp, int c,
+                                                   double s, double goal, double period, double idle) {
   Outcome o;
-  int stage = __float_as_int(T.cellB[c].w);
+  const int stage = __float_as_int(sB[c].w);
+  const int first = stage == 0 ? c : c - (stage - 1);
   double lat;
   if (stage == 0) {
-    double t = T.t64[c];
+    double t = C[c].t;
     lat = xmul(s, t);
     o.completed = lat <= goal ? 1 : 0;
     o.fb_latency = lat;
     o.fb_t_prof = t;
   } else {
-    int first = c - (stage - 1);
-    double stop = py_min(xmul(s, T.t64[c]), goal);
+    double stop = py_min(xmul(s, C[c].t), goal);
     int completed = 0;
     for (int m = 0; m < stage; ++m)
-      if (xmul(s, T.t64[first + m]) <= stop) completed = m + 1;
+      if (xmul(s, C[first + m].t) <= stop) completed = m + 1;
     o.completed = completed;
     lat = stop;
     if (completed) {
-      double t = T.t64[first + completed - 1];
+      double t = C[first + completed - 1].t;
       o.fb_latency = xmul(s, t);
       o.fb_t_prof = t;
     } else {
       o.fb_latency = stop;
-      o.fb_t_prof = T.t64[first];
+      o.fb_t_prof = C[first].t;
     }
   }
-  double cap = T.cap64[c];
-  o.latency = xadd(lat, sp->overhead_budget);
-  if (o.completed >= 1) {
-    int first = stage == 0 ? c : c - (stage - 1);
-    o.delivered = T.a64[first + o.completed - 1];
-  } else {
-    o.delivered = T.qf64[c];
-  }
+  const double cap = C[c].cap;
+  o.latency = xadd(lat, sp->oh);
+  o.delivered = o.completed >= 1 ? C[first + o.completed - 1].a : C[c].qf;
   o.met = o.completed >= 1 && o.latency <= period;
   o.energy = xadd(xmul(cap, py_min(o.latency, period)), xmul(idle, py_max(0.0, xsub(period, o.latency))));
   o.vl = !o.met;
@@ -562,11 +598,16 @@ struct Filter {
   double mu, sigma2, k_gain, q_noise, innov, phi, m_var;
 };
 
-__device__ __forceinline__ void slowdown_update(const AlertFilterConfig& cfg, Filter& f, double obs, double t_prof) {
+// k_valid: the previous update of this launch left k_gain = prior/(prior + r)
+// and sigma2 = prior (reference gain convention), so an unchanged prior (the
+// filter's fixed point whenever Q sits at its floor) reuses k_gain exactly
+// instead of dividing again.
+__device__ __forceinline__ void slowdown_update(const AlertFilterConfig& cfg, Filter& f, double obs, double t_prof,
+                                                bool& k_valid) {
   double ky = xmul(f.k_gain, f.innov);
   double q = py_max(cfg.q0, xadd(xmul(cfg.alpha, f.q_noise), xmul(xsub(1.0, cfg.alpha), xmul(ky, ky))));
   double prior = xadd(xmul(xsub(1.0, f.k_gain), f.sigma2), q);
-  double k = xdiv(prior, xadd(prior, cfg.r));
+  double k = (k_valid && prior == f.sigma2) ? f.k_gain : xdiv(prior, xadd(prior, cfg.r));
   double y = xsub(xdiv(obs, t_prof), f.mu);
   double mu = xadd(f.mu, xmul(k, y));
   double s2 = cfg.sigma2_uses_current_gain ? xadd(xmul(xsub(1.0, k), f.sigma2), q) : prior;
@@ -575,13 +616,24 @@ __device__ __forceinline__ void slowdown_update(const AlertFilterConfig& cfg, Fi
   f.k_gain = k;
   f.q_noise = q;
   f.innov = y;
+  k_valid = !cfg.sigma2_uses_current_gain;
 }
 
-__device__ __forceinline__ void idle_update(const AlertFilterConfig& cfg, Filter& f, double measured, double cap) {
-  double ratio = py_min(1.0, xdiv(measured, cap));
-  double ms = xadd(f.m_var, cfg.s);
-  double w = xdiv(ms, xadd(ms, cfg.v));
-  f.m_var = xmul(xsub(1.0, w), ms);
+// ratio = min(1, measured / cap) is supplied by the caller (per-segment
+// table).  The gain W depends only on M, whose sequence from m0 is the same
+// for every stream: position ik in the host-computed table (ik < 0: divide).
+__device__ __forceinline__ void idle_update(const AlertFilterConfig& cfg, Filter& f, double ratio, int& ik,
+                                            int fix, const double* tw, const double* tm) {
+  double w;
+  if (ik >= 0) {
+    w = tw[ik];
+    if (ik < fix) ++ik;
+    f.m_var = tm[ik];
+  } else {
+    double ms = xadd(f.m_var, cfg.s);
+    w = xdiv(ms, xadd(ms, cfg.v));
+    f.m_var = xmul(xsub(1.0, w), ms);
+  }
   f.phi = xadd(f.phi, xmul(w, xsub(ratio, f.phi)));
 }
 
@@ -589,21 +641,22 @@ __device__ __forceinline__ void idle_update(const AlertFilterConfig& cfg, Filter
 // OraclePolicy.decide (policies.py:160-205): exact per-cell outcome under the
 // true slow-down, three fallback levels at once, FP64.
 template <class Tile>
-__device__ Decision oracle_decide(const DevTable& T, const Tile& tile, const AlertSpec* sp, double s,
+__device__ Decision oracle_decide(const DevTable& T, const float4* sB, const Cell64* C, const int2* sCol,
+                                  const Tile& tile, const SpecDev* sp, double s,
                                   double idle, double goal) {
   const int W = Tile::num_threads();
   const int lane = tile.thread_rank();
-  const double oh = sp->overhead_budget;
+  const double oh = sp->oh;
   const double period = xadd(goal, oh);
   const bool maxacc = sp->mode == ALERT_MODE_MAX_ACCURACY;
   Key64 best[3];
   best[0].init(); best[1].init(); best[2].init();
   auto consider = [&](int c, int completed, double lat_raw, double delivered) {
-    double cap = T.cap64[c];
+    double cap = C[c].cap;
     double L = xadd(lat_raw, oh);
     bool met = completed >= 1 && L <= period;
     double E = xadd(xmul(cap, py_min(L, period)), xmul(idle, py_max(0.0, xsub(period, L))));
-    uint32_t tk = __float_as_uint(T.cellB[c].y);
+    uint32_t tk = __float_as_uint(sB[c].y);
 #pragma unroll
     for (int lvl = 0; lvl < 3; ++lvl) {
       if (lvl != 2 && !met) continue;
@@ -622,18 +675,18 @@ __device__ Decision oracle_decide(const DevTable& T, const Tile& tile, const Ale
     }
   };
   for (int c = lane; c < T.n_trad; c += W) {
-    double lat = xmul(s, T.t64[c]);
+    double lat = xmul(s, C[c].t);
     bool done = lat <= goal;
-    consider(c, done ? 1 : 0, lat, done ? T.a64[c] : T.qf64[c]);
+    consider(c, done ? 1 : 0, lat, done ? C[c].a : C[c].qf);
   }
   for (int col = lane; col < T.n_any_cols; col += W) {
-    int2 cd = T.any_cols[col];
+    int2 cd = sCol[col];
     int K = 0;
-    double deliv = T.qf64[cd.x];
+    double deliv = C[cd.x].qf;
     for (int k = 0; k < cd.y; ++k) {
       int c = cd.x + k;
-      double st = xmul(s, T.t64[c]);
-      if (st <= goal) { K = k + 1; deliv = T.a64[c]; }
+      double st = xmul(s, C[c].t);
+      if (st <= goal) { K = k + 1; deliv = C[c].a; }
       consider(c, K, py_min(st, goal), deliv);
     }
   }

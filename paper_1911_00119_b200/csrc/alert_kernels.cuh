@@ -8,10 +8,15 @@
 
 namespace alert {
 
+constexpr int kIdleTab = 96;       // entries of the idle-filter gain table
+constexpr int kSpecSmemMax = 64;   // specs staged in shared memory up to this count
+constexpr int kC64SmemMax = 1024;  // FP64 cell rows staged in shared memory up to this count
+constexpr int kRatioSmemMax = 64;  // powers of the per-segment idle-ratio table
+
 struct RunParams {
   DevTable T;
   AlertFilterConfig cfg;
-  const AlertSpec* specs;
+  const SpecDev* specs;
   int n_specs;
   const int32_t* stream_spec;
   AlertTrace tr;
@@ -20,7 +25,31 @@ struct RunParams {
   int policy;
   unsigned flags;
   int kinds;
+  int spec_smem, c64_smem, ratio_smem;  // staging decisions (host computed)
   long long stream_begin, stream_end, step_begin, step_end;
+  // Idle-filter gains (estimator.py:123-125) do not depend on the data: the
+  // sequence M_k (state after k updates from m0) and W_k reaches an exact FP64
+  // fixed point at k = idle_fix; M/W are precomputed on the host with the
+  // reference's operations.  idle_fix < 0: table unused (division path).
+  int idle_fix;
+  double idle_w[kIdleTab];
+  double idle_m[kIdleTab];
+};
+
+// Shared-memory layout of run_kernel (host and device compute it identically).
+struct SmemLayout {
+  size_t B, col, spec, c64, ratio, agg, total;
+  __host__ __device__ static size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
+  __host__ __device__ SmemLayout(int n_cells, int n_cols, int n_spec, int n_c64, int n_tiles, int n_ratio,
+                                 size_t agg_bytes) {
+    B = sizeof(float4) * (size_t)n_cells;
+    col = B + sizeof(float4) * (size_t)n_cells;
+    spec = up16(col + sizeof(int2) * (size_t)(n_cols + 1));
+    c64 = up16(spec + sizeof(SpecDev) * (size_t)n_spec);
+    ratio = up16(c64 + sizeof(Cell64) * (size_t)n_c64);
+    agg = up16(ratio + sizeof(double) * (size_t)n_tiles * (size_t)n_ratio);
+    total = up16(agg + agg_bytes * (size_t)n_tiles);
+  }
 };
 
 __device__ __forceinline__ void load_table_smem(const DevTable& T, float4* sA, float4* sB, int2* sCol) {
@@ -29,33 +58,65 @@ __device__ __forceinline__ void load_table_smem(const DevTable& T, float4* sA, f
     sB[i] = T.cellB[i];
   }
   for (int i = threadIdx.x; i < T.n_any_cols; i += blockDim.x) sCol[i] = T.any_cols[i];
-  __syncthreads();
 }
 
-__device__ __forceinline__ double load_s(const AlertTrace& tr, long long row, long long n) {
+// The trace value is prefetched one step ahead as RAW bits and converted only
+// when consumed, so the load latency overlaps a whole step of scan work.
+__device__ __forceinline__ unsigned long long load_s_raw(const AlertTrace& tr, long long row, long long n) {
   const long long off = row * tr.row_stride + (n - tr.step_offset) * tr.step_stride;
-  if (tr.slowdown_dtype == ALERT_DTYPE_F64) return __ldg(reinterpret_cast<const double*>(tr.slowdown) + off);
-  return (double)__ldg(reinterpret_cast<const float*>(tr.slowdown) + off);
+  if (tr.slowdown_dtype == ALERT_DTYPE_F64)
+    return __ldg(reinterpret_cast<const unsigned long long*>(tr.slowdown) + off);
+  return __ldg(reinterpret_cast<const unsigned int*>(tr.slowdown) + off);
+}
+__device__ __forceinline__ double s_of_raw(const AlertTrace& tr, unsigned long long raw) {
+  return tr.slowdown_dtype == ALERT_DTYPE_F64 ? __longlong_as_double((long long)raw)
+                                              : (double)__uint_as_float((unsigned int)raw);
 }
 
-// Per-tile FP64 accumulators, kept in shared memory: they are touched once
-// per step (not per candidate), so they need not occupy registers.
+// Per-tile accumulators in shared memory (touched once per step by the tile's
+// writer lane, never per candidate).  Float sums are Neumaier pairs (CPython
+// 3.12 sum()); counts are int deltas since the current segment started.
 struct TileAgg {
-  double e, ec, a, ac;          // Neumaier sums of energy / delivered accuracy
-  double pn, pe, pec, pa, pac;  // current phase: count, sums
-  double pvl, pva, pve;         // current phase violation counts
-  double oe, oec, oa, oac;      // oracle-alongside sums
+  double e, ec, a, ac;      // overall energy / delivered accuracy
+  double pe, pec, pa, pac;  // current phase (loaded / stored at segment changes)
+  double oe, oec, oa, oac;  // oracle alongside
+  int dn, dvl, dva, dve;    // current segment counts
+  int l1, l2, ref, osame;   // launch totals
+  int ovl, ova, ove, pad;
 };
 
 enum { PF_ALERT = 0, PF_ORACLE = 1, PF_BOTH = 2 };  // policy families
 
-__device__ __forceinline__ void load_phase(TileAgg& g, const double* agg, int phase) {
-  const double* p = agg + ALERT_AGG_PHASE_BASE + ALERT_AGG_PHASE_STRIDE * phase;
-  g.pn = p[0]; g.pe = p[1]; g.pec = p[2]; g.pa = p[3]; g.pac = p[4]; g.pvl = p[5]; g.pva = p[6]; g.pve = p[7];
+// Close the current segment: per-phase slot (phase ids < ALERT_MAX_PHASES) and
+// overall violation counts.
+__device__ __forceinline__ void flush_segment(TileAgg& g, double* agg, int phase) {
+  if (phase >= 0 && phase < ALERT_MAX_PHASES) {
+    double* p = agg + ALERT_AGG_PHASE_BASE + ALERT_AGG_PHASE_STRIDE * phase;
+    p[0] += (double)g.dn;
+    p[1] = g.pe; p[2] = g.pec; p[3] = g.pa; p[4] = g.pac;
+    p[5] += (double)g.dvl; p[6] += (double)g.dva; p[7] += (double)g.dve;
+  }
+  agg[ALERT_AGG_VIOL_LAT] += (double)g.dvl;
+  agg[ALERT_AGG_VIOL_ACC] += (double)g.dva;
+  agg[ALERT_AGG_VIOL_ENERGY] += (double)g.dve;
+  g.dn = g.dvl = g.dva = g.dve = 0;
 }
-__device__ __forceinline__ void store_phase(const TileAgg& g, double* agg, int phase) {
-  double* p = agg + ALERT_AGG_PHASE_BASE + ALERT_AGG_PHASE_STRIDE * phase;
-  p[0] = g.pn; p[1] = g.pe; p[2] = g.pec; p[3] = g.pa; p[4] = g.pac; p[5] = g.pvl; p[6] = g.pva; p[7] = g.pve;
+__device__ __forceinline__ void open_segment(TileAgg& g, const double* agg, int phase) {
+  if (phase >= 0 && phase < ALERT_MAX_PHASES) {
+    const double* p = agg + ALERT_AGG_PHASE_BASE + ALERT_AGG_PHASE_STRIDE * phase;
+    g.pe = p[1]; g.pec = p[2]; g.pa = p[3]; g.pac = p[4];
+  } else {
+    g.pe = g.pec = g.pa = g.pac = 0.0;
+  }
+}
+
+// min(1, idle / cap) for every power of the current segment (estimator.py:123),
+// lanes of the tile split the powers.
+template <class Tile>
+__device__ __forceinline__ void fill_ratios(const DevTable& T, const Tile& tile, double* r, double idle) {
+  for (int j = tile.thread_rank(); j < T.n_powers; j += Tile::num_threads())
+    r[j] = py_min(1.0, xdiv(idle, T.power_cap64[j]));
+  tile.sync();
 }
 
 // The fused closed loop (simulator.run, simulator.py:461-507): one tile of W
@@ -64,20 +125,34 @@ template <int W, int PF>
 __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   extern __shared__ float4 smem[];
   const DevTable& T = P.T;
+  const int n_tiles = blockDim.x / W;
+  const SmemLayout L(T.n_cells, T.n_any_cols, P.spec_smem ? P.n_specs : 0, P.c64_smem ? T.n_cells : 0, n_tiles,
+                     P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg));
+  char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
-  float4* sB = smem + T.n_cells;
-  int2* sCol = reinterpret_cast<int2*>(sB + T.n_cells);
-  TileAgg* sAgg = reinterpret_cast<TileAgg*>(sCol + T.n_any_cols + 1);
+  float4* sB = reinterpret_cast<float4*>(base + L.B);
+  int2* sCol = reinterpret_cast<int2*>(base + L.col);
+  SpecDev* sSpec = reinterpret_cast<SpecDev*>(base + L.spec);
+  Cell64* sC64 = reinterpret_cast<Cell64*>(base + L.c64);
+  double* sRatio = reinterpret_cast<double*>(base + L.ratio);
+  TileAgg* sAgg = reinterpret_cast<TileAgg*>(base + L.agg);
   load_table_smem(T, sA, sB, sCol);
+  if (P.spec_smem)
+    for (int i = threadIdx.x; i < P.n_specs; i += blockDim.x) sSpec[i] = P.specs[i];
+  if (P.c64_smem)
+    for (int i = threadIdx.x; i < T.n_cells; i += blockDim.x) sC64[i] = T.c64[i];
+  __syncthreads();
+  const Cell64* C64 = P.c64_smem ? sC64 : T.c64;
 
   auto tile = cg::tiled_partition<W>(cg::this_thread_block());
   const long long stream = P.stream_begin + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;
   if (stream >= P.stream_end) return;
   const bool writer = tile.thread_rank() == 0;
   TileAgg& G = sAgg[threadIdx.x / W];
+  double* ratio_tab = P.ratio_smem ? sRatio + (size_t)(threadIdx.x / W) * T.n_powers : nullptr;
 
   const int si = P.stream_spec ? P.stream_spec[stream] : (int)(stream % P.n_specs);
-  const AlertSpec* spec = P.specs + si;
+  const SpecDev* spec = P.spec_smem ? sSpec + si : P.specs + si;
   const AlertTrace& tr = P.tr;
   const long long row = tr.stream_row ? tr.stream_row[stream] : stream;
 
@@ -89,6 +164,11 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   f.innov = P.st.innov[stream];
   f.phi = P.st.phi[stream];
   f.m_var = P.st.m_var[stream];
+  bool k_valid = false;  // k_gain == sigma2 / (sigma2 + r) holds after one update here
+  int ik = -1;           // position in the idle-filter gain table
+  if (P.idle_fix >= 0)
+    for (int k = 0; k <= P.idle_fix; ++k)
+      if (P.idle_m[k] == f.m_var) { ik = k; break; }
   double budget = P.st.group_budget[stream];
   int count = P.st.group_count[stream];
   const int group_size = spec->group_size;
@@ -103,21 +183,18 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   int cur_end = seg_end[seg];
   int phase = seg_phase[seg];
   double idle = seg_idle[seg];
+  if (ratio_tab) fill_ratios(T, tile, ratio_tab, idle);
 
   double* agg = P.out.agg ? P.out.agg + stream * ALERT_AGG_FIELDS : nullptr;
-  int cVL = 0, cVA = 0, cVE = 0, cL1 = 0, cL2 = 0, cRef = 0;
-  int oVL = 0, oVA = 0, oVE = 0, oSame = 0;
-  if (writer) {
+  if (writer && agg) {
     G = TileAgg{};
-    if (agg) {
-      G.e = agg[ALERT_AGG_ENERGY]; G.ec = agg[ALERT_AGG_ENERGY_C];
-      G.a = agg[ALERT_AGG_ACC]; G.ac = agg[ALERT_AGG_ACC_C];
-      if (PF == PF_BOTH) {
-        G.oe = agg[ALERT_AGG_OR_ENERGY]; G.oec = agg[ALERT_AGG_OR_ENERGY_C];
-        G.oa = agg[ALERT_AGG_OR_ACC]; G.oac = agg[ALERT_AGG_OR_ACC_C];
-      }
-      if (phase >= 0 && phase < ALERT_MAX_PHASES) load_phase(G, agg, phase);
+    G.e = agg[ALERT_AGG_ENERGY]; G.ec = agg[ALERT_AGG_ENERGY_C];
+    G.a = agg[ALERT_AGG_ACC]; G.ac = agg[ALERT_AGG_ACC_C];
+    if (PF == PF_BOTH) {
+      G.oe = agg[ALERT_AGG_OR_ENERGY]; G.oec = agg[ALERT_AGG_OR_ENERGY_C];
+      G.oa = agg[ALERT_AGG_OR_ACC]; G.oac = agg[ALERT_AGG_OR_ACC_C];
     }
+    open_segment(G, agg, phase);
   }
 
   const int kinds = P.kinds;
@@ -125,66 +202,67 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   const bool no_refine = P.flags & ALERT_FLAG_NO_REFINE;
   const int* forced = P.out.forced;
 
-  double s_next = load_s(tr, row, P.step_begin);
+  unsigned long long s_next = load_s_raw(tr, row, P.step_begin);
   for (long long n = P.step_begin; n < P.step_end; ++n) {
-    const double s = s_next;
-    if (n + 1 < P.step_end) s_next = load_s(tr, row, n + 1);
-    while (seg + 1 < nseg && n >= cur_end) {
-      if (agg && writer && phase >= 0 && phase < ALERT_MAX_PHASES) store_phase(G, agg, phase);
-      ++seg;
-      cur_end = seg_end[seg];
+    const unsigned long long s_raw = s_next;
+    if (n + 1 < P.step_end) s_next = load_s_raw(tr, row, n + 1);
+    if (n >= cur_end && seg + 1 < nseg) {
+      if (agg && writer) flush_segment(G, agg, phase);
+      while (seg + 1 < nseg && n >= cur_end) {
+        ++seg;
+        cur_end = seg_end[seg];
+      }
       phase = seg_phase[seg];
       idle = seg_idle[seg];
-      if (writer) {
-        if (agg && phase >= 0 && phase < ALERT_MAX_PHASES) load_phase(G, agg, phase);
-        else G.pn = G.pe = G.pec = G.pa = G.pac = G.pvl = G.pva = G.pve = 0.0;
-      }
+      if (ratio_tab) fill_ratios(T, tile, ratio_tab, idle);
+      if (agg && writer) open_segment(G, agg, phase);
     }
     // adjust_goal (selector.py:48-70) with group budgets (simulator.py:473-483)
-    const double oh = spec->overhead_budget;
-    double goal;
+    double goal, period;
     if (group_size > 0) {
       if (count == 0) {
         budget = xmul((double)group_size, spec->t_goal);
         count = group_size;
       }
-      goal = xsub(xdiv(budget, (double)count), oh);
+      goal = py_max(xsub(xdiv(budget, (double)count), spec->oh), 0.001);
+      period = xadd(goal, spec->oh);
     } else {
-      goal = xsub(spec->t_goal, oh);
+      goal = spec->goal0;
+      period = spec->period0;
     }
-    goal = py_max(goal, 0.001);
-    const double period = xadd(goal, oh);
 
     Decision d;
+    double s;  // true slow-down of this input: consumed only after the decision
     if (PF == PF_ORACLE) {
-      d = oracle_decide(T, tile, spec, s, idle, goal);
+      s = s_of_raw(tr, s_raw);
+      d = oracle_decide(T, sB, C64, sCol, tile, spec, s, idle, goal);
       d.refined = false;
     } else {
       StepCtx x;
-      make_ctx(x, spec, f.mu, f.sigma2, f.phi, goal, fp64_all);
+      make_ctx(x, spec, C64, f.mu, f.sigma2, f.phi, goal, fp64_all);
       d = alert_decide(T, sA, sB, sCol, tile, x, kinds, no_refine);
+      s = s_of_raw(tr, s_raw);
     }
     int exec_cell = d.cell;
-    const long long oidx = stream * P.out.stream_stride + n * P.out.step_stride;
     if (forced) {
-      int fc = forced[oidx];
+      const int fc = forced[stream * P.out.stream_stride + n * P.out.step_stride];
       if (fc >= 0) exec_cell = T.cell_of_cand[fc];
     }
-    const Outcome o = execute_measure(T, spec, exec_cell, s, goal, period, idle);
+    const Outcome o = execute_measure(sB, C64, spec, exec_cell, s, goal, period, idle);
     if (PF != PF_ORACLE) {  // AlertPolicy.observe, policies.py:105-108
-      slowdown_update(P.cfg, f, o.fb_latency, o.fb_t_prof);
-      idle_update(P.cfg, f, idle, T.cap64[exec_cell]);
+      slowdown_update(P.cfg, f, o.fb_latency, o.fb_t_prof, k_valid);
+      const int pw = __float_as_uint(sB[exec_cell].y) >> 20;  // power index from the tie key
+      const double ratio = ratio_tab ? ratio_tab[pw] : py_min(1.0, xdiv(idle, C64[exec_cell].cap));
+      idle_update(P.cfg, f, ratio, ik, P.idle_fix, P.idle_w, P.idle_m);
     }
     if (group_size > 0) {  // simulator.py:501-503
       budget = xsub(budget, o.latency);
       count -= 1;
     }
-    cVL += o.vl; cVA += o.va; cVE += o.ve;
-    cL1 += d.level == 1; cL2 += d.level == 2;
-    cRef += d.refined;
-    if (writer) {
-      const AlertOutputs& out = P.out;
-      if (out.decision) out.decision[oidx] = pack_decision(__float_as_int(sB[d.cell].z), d.level, o, d.refined, phase);
+    const AlertOutputs& out = P.out;
+    if (writer && out.decision) {
+      const long long oidx = stream * out.stream_stride + n * out.step_stride;
+      out.decision[oidx] = pack_decision(__float_as_int(sB[d.cell].z), d.level, o, d.refined, phase);
       if (out.record_dtype == ALERT_DTYPE_F64) {
         if (out.energy) static_cast<double*>(out.energy)[oidx] = o.energy;
         if (out.accuracy) static_cast<double*>(out.accuracy)[oidx] = o.delivered;
@@ -198,25 +276,29 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
         if (out.mu) static_cast<float*>(out.mu)[oidx] = (float)f.mu;
         if (out.sigma2) static_cast<float*>(out.sigma2)[oidx] = (float)f.sigma2;
       }
-      // aggregates in step order (CPython 3.12 sum() semantics)
+    }
+    if (writer && agg) {  // aggregates in step order (CPython 3.12 sum() semantics)
       neumaier(G.e, G.ec, o.energy);
       neumaier(G.a, G.ac, o.delivered);
-      G.pn += 1.0;
       neumaier(G.pe, G.pec, o.energy);
       neumaier(G.pa, G.pac, o.delivered);
-      G.pvl += o.vl; G.pva += o.va; G.pve += o.ve;
+      G.dn += 1;
+      G.dvl += o.vl; G.dva += o.va; G.dve += o.ve;
+      G.l1 += d.level == 1; G.l2 += d.level == 2;
+      G.ref += d.refined;
     }
     if (PF == PF_BOTH) {  // OraclePolicy alongside on the same step
-      Decision od = oracle_decide(T, tile, spec, s, idle, goal);
-      const Outcome oo = execute_measure(T, spec, od.cell, s, goal, period, idle);
-      oVL += oo.vl; oVA += oo.va; oVE += oo.ve;
-      oSame += od.cell == exec_cell;
-      if (writer) {
+      Decision od = oracle_decide(T, sB, C64, sCol, tile, spec, s, idle, goal);
+      const Outcome oo = execute_measure(sB, C64, spec, od.cell, s, goal, period, idle);
+      if (writer && agg) {
         neumaier(G.oe, G.oec, oo.energy);
         neumaier(G.oa, G.oac, oo.delivered);
-        if (P.out.oracle_decision)
-          P.out.oracle_decision[oidx] = pack_decision(__float_as_int(sB[od.cell].z), od.level, oo, false, phase);
+        G.ovl += oo.vl; G.ova += oo.va; G.ove += oo.ve;
+        G.osame += od.cell == exec_cell;
       }
+      if (writer && out.oracle_decision)
+        out.oracle_decision[stream * out.stream_stride + n * out.step_stride] =
+            pack_decision(__float_as_int(sB[od.cell].z), od.level, oo, false, phase);
     }
   }
   if (!writer) return;
@@ -230,25 +312,22 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   P.st.group_budget[stream] = budget;
   P.st.group_count[stream] = count;
   if (agg) {
-    if (phase >= 0 && phase < ALERT_MAX_PHASES) store_phase(G, agg, phase);
+    flush_segment(G, agg, phase);
     const double steps = (double)(P.step_end - P.step_begin);
     agg[ALERT_AGG_N] += steps;
     agg[ALERT_AGG_ENERGY] = G.e; agg[ALERT_AGG_ENERGY_C] = G.ec;
     agg[ALERT_AGG_ACC] = G.a; agg[ALERT_AGG_ACC_C] = G.ac;
-    agg[ALERT_AGG_VIOL_LAT] += (double)cVL;
-    agg[ALERT_AGG_VIOL_ACC] += (double)cVA;
-    agg[ALERT_AGG_VIOL_ENERGY] += (double)cVE;
-    agg[ALERT_AGG_LEVEL0] += steps - (double)cL1 - (double)cL2;
-    agg[ALERT_AGG_LEVEL1] += (double)cL1;
-    agg[ALERT_AGG_LEVEL2] += (double)cL2;
-    agg[ALERT_AGG_REFINED] += (double)cRef;
+    agg[ALERT_AGG_LEVEL0] += steps - (double)G.l1 - (double)G.l2;
+    agg[ALERT_AGG_LEVEL1] += (double)G.l1;
+    agg[ALERT_AGG_LEVEL2] += (double)G.l2;
+    agg[ALERT_AGG_REFINED] += (double)G.ref;
     if (PF == PF_BOTH) {
       agg[ALERT_AGG_OR_ENERGY] = G.oe; agg[ALERT_AGG_OR_ENERGY_C] = G.oec;
       agg[ALERT_AGG_OR_ACC] = G.oa; agg[ALERT_AGG_OR_ACC_C] = G.oac;
-      agg[ALERT_AGG_OR_VIOL_LAT] += (double)oVL;
-      agg[ALERT_AGG_OR_VIOL_ACC] += (double)oVA;
-      agg[ALERT_AGG_OR_VIOL_ENERGY] += (double)oVE;
-      agg[ALERT_AGG_OR_SAME] += (double)oSame;
+      agg[ALERT_AGG_OR_VIOL_LAT] += (double)G.ovl;
+      agg[ALERT_AGG_OR_VIOL_ACC] += (double)G.ova;
+      agg[ALERT_AGG_OR_VIOL_ENERGY] += (double)G.ove;
+      agg[ALERT_AGG_OR_SAME] += (double)G.osame;
     }
   }
 }
@@ -256,7 +335,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
 struct StepParams {
   DevTable T;
   AlertFilterConfig cfg;
-  const AlertSpec* specs;
+  const SpecDev* specs;
   int n_specs;
   const int32_t* stream_spec;
   AlertState st;
@@ -276,28 +355,28 @@ __global__ void __launch_bounds__(256) decide_kernel(const StepParams P, uint32_
   float4* sB = smem + T.n_cells;
   int2* sCol = reinterpret_cast<int2*>(sB + T.n_cells);
   load_table_smem(T, sA, sB, sCol);
+  __syncthreads();
   auto tile = cg::tiled_partition<W>(cg::this_thread_block());
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;
   if (i >= P.n) return;
   const int si = P.stream_spec ? P.stream_spec[i] : (int)(i % P.n_specs);
-  const AlertSpec spec = P.specs[si];
+  const SpecDev* spec = P.specs + si;
   StepCtx x;
-  make_ctx(x, &spec, P.st.mu[i], P.st.sigma2[i], P.st.phi[i], P.goal[i], P.flags & ALERT_FLAG_FP64_ALL);
+  make_ctx(x, spec, T.c64, P.st.mu[i], P.st.sigma2[i], P.st.phi[i], P.goal[i], P.flags & ALERT_FLAG_FP64_ALL);
   Decision d = alert_decide(T, sA, sB, sCol, tile, x, P.kinds, P.flags & ALERT_FLAG_NO_REFINE);
   if (tile.thread_rank() == 0)
     decision[i] = (uint32_t)__float_as_int(sB[d.cell].z) | ((uint32_t)d.level << 16) | ((uint32_t)d.refined << 26);
 }
 
 template <int W>
-__global__ void oracle_decide_kernel(const DevTable T, const AlertSpec* specs, int n_specs, const int32_t* stream_spec,
+__global__ void oracle_decide_kernel(const DevTable T, const SpecDev* specs, int n_specs, const int32_t* stream_spec,
                                      const double* s, const double* idle, const double* goal, uint32_t* decision,
                                      long long n) {
   auto tile = cg::tiled_partition<W>(cg::this_thread_block());
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;
   if (i >= n) return;
   const int si = stream_spec ? stream_spec[i] : (int)(i % n_specs);
-  const AlertSpec spec = specs[si];
-  Decision d = oracle_decide(T, tile, &spec, s[i], idle[i], goal[i]);
+  Decision d = oracle_decide(T, T.cellB, T.c64, T.any_cols, tile, specs + si, s[i], idle[i], goal[i]);
   if (tile.thread_rank() == 0) decision[i] = (uint32_t)__float_as_int(T.cellB[d.cell].z) | ((uint32_t)d.level << 16);
 }
 
@@ -308,7 +387,7 @@ cudaError_t launch_run(int pf, const RunParams& P, int tpb, size_t smem, cudaStr
 template <int W>
 cudaError_t launch_decide(const StepParams& P, uint32_t* out, int tpb, size_t smem, cudaStream_t st);
 template <int W>
-cudaError_t launch_oracle(const DevTable& T, const AlertSpec* specs, int n_specs, const int32_t* stream_spec,
+cudaError_t launch_oracle(const DevTable& T, const SpecDev* specs, int n_specs, const int32_t* stream_spec,
                           const double* s, const double* idle, const double* goal, uint32_t* decision,
                           long long n, int tpb, cudaStream_t st);
 
@@ -344,7 +423,7 @@ inline cudaError_t set_smem(K kern, size_t smem) {
     return cudaGetLastError();                                                                        \
   }                                                                                                   \
   template <>                                                                                         \
-  cudaError_t launch_oracle<W>(const DevTable& T, const AlertSpec* specs, int n_specs,                \
+  cudaError_t launch_oracle<W>(const DevTable& T, const SpecDev* specs, int n_specs,                  \
                                const int32_t* stream_spec, const double* s, const double* idle,       \
                                const double* goal, uint32_t* decision, long long n, int tpb,         \
                                cudaStream_t st) {                                                     \
