@@ -396,7 +396,7 @@ static int kinds_of(int policy, const AlertTable* tb) {
 }
 
 static size_t table_smem(const AlertTable* tb) {
-  return sizeof(float4) * 2 * (size_t)tb->dev.n_cells + sizeof(int2) * (size_t)(tb->dev.n_any_cols + 1);
+  return SmemLayout(tb->dev.n_cells, tb->dev.n_any_cols, 0, 0, 0, 0, 0).total;
 }
 
 // Staging decisions of run_kernel: specs, FP64 cells and the per-segment
@@ -407,12 +407,13 @@ static void run_staging(const AlertTable* tb, int n_specs, int tpb, int W, RunPa
   P.c64_smem = T.n_cells <= kC64SmemMax;
   P.ratio_smem = T.n_powers <= kRatioSmemMax &&
                  (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;
+  P.sv_smem = (size_t)(tpb / W) * (size_t)T.n_cells * sizeof(float) <= 32 * 1024;
 }
 
 static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const RunParams& P) {
   const DevTable& T = tb->dev;
   SmemLayout L(T.n_cells, T.n_any_cols, P.spec_smem ? n_specs : 0, P.c64_smem ? T.n_cells : 0, tpb / W,
-               P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg));
+               P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0);
   return L.total;
 }
 

@@ -84,14 +84,16 @@ __device__ __forceinline__ void neumaier(double& s, double& c, double x) {
   s = t;
 }
 
-// Standard normal CDF in FP32 from x = z / sqrt(2):
-//   erfc(a) = t * exp(-a^2 + P(t)),  t = 1 / (1 + a/2),  a = |x|
-// (rational-exponential form with a degree-9 polynomial; relative error
-// <= 1.2e-7 over a >= 0), Phi = 1 - erfc(a)/2 for x >= 0 else erfc(a)/2.
-// One branch-free formula: 1 FFMA + RCP + 9 FFMA (immediate coefficients) +
-// 2 FFMA + EX2 + FMUL + FADD/FSEL.  Absolute error bound used by the
-// near-tie logic: ALERT_PHI32_ERR (checked on the GPU, tests/test_gpu_parity.py).
+// Standard normal CDF in FP32 from x = z / sqrt(2): Phi = 1 - erfc(a)/2 for
+// x >= 0 else erfc(a)/2, a = |x>, one branch-free formula (phi32_x below):
+// FFMA + RCP + 4 FFMA (immediate coefficients) + FMUL + FFMA + EX2 + 2 FMUL +
+// FADD/FSEL.  Absolute error bound used by the near-tie logic (checked on the
+// GPU against FP64, tests/test_gpu_parity.py::test_phi32_error_bound):
 #define ALERT_PHI32_ERR_EPS 4.0f  // in units of 2^-23
+// Shared-memory padding (rows of the FP32 cell table and column descriptors)
+// that lets look-ahead loads run past the end without clamping: 2 chunks of 4
+// cells at the widest tile (32 lanes).
+#define ALERT_SMEM_PAD 256
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -102,20 +104,19 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// Abramowitz & Stegun 7.1.26: erfc(a) = t (a1 + t(a2 + t(a3 + t(a4 + t a5)))) e^{-a^2},
+// t = 1/(1 + p a), |error| <= 1.5e-7 absolute — absolute accuracy is all the
+// scan needs (probabilities enter accuracies and thresholds additively).
 __device__ __forceinline__ float phi32_x(float x) {
   const float a = fabsf(x);
-  const float t = rcp_approx(fmaf(0.5f, a, 1.0f));
-  float p = fmaf(t, 0.17087277f, -0.82215223f);
-  p = fmaf(t, p, 1.48851587f);
-  p = fmaf(t, p, -1.13520398f);
-  p = fmaf(t, p, 0.27886807f);
-  p = fmaf(t, p, -0.18628806f);
-  p = fmaf(t, p, 0.09678418f);
-  p = fmaf(t, p, 0.37409196f);
-  p = fmaf(t, p, 1.00002368f);
-  p = fmaf(t, p, -1.26551223f);
-  const float arg = fmaf(-a, a, p);                                    // ln(erfc(a) / t)
-  const float h = t * ex2_approx(fmaf(arg, 1.44269504088896341f, -1.0f));  // erfc(a) / 2
+  const float t = rcp_approx(fmaf(0.3275911f, a, 1.0f));
+  float p = fmaf(t, 1.061405429f, -1.453152027f);
+  p = fmaf(t, p, 1.421413741f);
+  p = fmaf(t, p, -0.284496736f);
+  p = fmaf(t, p, 0.254829592f);
+  const float al = a * 1.44269504088896341f;
+  const float e = ex2_approx(fmaf(-al, a, -1.0f));  // e^{-a^2} / 2
+  const float h = (p * t) * e;                      // erfc(a) / 2
   return x >= 0.0f ? 1.0f - h : h;
 }
 
@@ -143,6 +144,7 @@ struct StepCtx {
   // thresholds with margins
   float q_hi, q_lo, th_hi, th_lo, e_hi, e_lo;
   bool fp64_all;
+  float* sv;  // per-tile FP32 objective of every cell (shared memory) or nullptr
 };
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -157,6 +159,7 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
                                          double sigma2, double phi, double goal, bool fp64_all) {
   x.spec = sp;
   x.c64 = c64;
+  x.sv = nullptr;
   x.mu = mu;
   x.sig = sigma2;  // holds sigma2 until ensure_fp64()
   x.phi = phi;
@@ -356,10 +359,15 @@ struct AlertScan {
     float v;
     classify(x, 0, pr, acc, E, s, p, v);
     t[0].push(v, s, p && !s, c);
+    bool p1 = false;
     if (MODE == ALERT_MODE_MAX_ACCURACY) {
-      classify(x, 1, pr, acc, E, s, p, v);
-      t[1].push(v, s, p && !s, c);
+      classify(x, 1, pr, acc, E, s, p1, v);
+      t[1].push(v, s, p1 && !s, c);
     }
+    // keep the level-0 objective (min-energy: E; max-accuracy: -acc, the same
+    // for every level) with the "possible" bits of levels 0/1 in its two low
+    // mantissa bits, for the re-rank pass
+    if (x.sv) x.sv[c] = __uint_as_float((__float_as_uint(v) & ~3u) | (unsigned)p | ((unsigned)p1 << 1));
   }
 
   __device__ __forceinline__ void refine_cell(const DevTable& T, const StepCtx& x, int c, float pr,
@@ -404,33 +412,35 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
   const int W = Tile::num_threads();
   const int lane = tile.thread_rank();
   const bool skip32 = PASS == 1 && S.all;
-  // Traditional cells: U cells per iteration, their table rows loaded one
-  // iteration ahead (register double buffer) so the shared-memory latency is
-  // off the critical path.  Indices are clamped for the look-ahead loads;
-  // out-of-range slots are not processed.
+  // Traditional cells, U per chunk.  Two register sets (a, b) ping-pong so the
+  // rows of the next chunk are loaded while the current one is evaluated,
+  // without register copies; the shared table is padded by ALERT_SMEM_PAD rows
+  // so look-ahead loads need no clamping.  Full double chunks first, then the
+  // remainder one cell at a time.
   const int n = T.n_trad;
   if ((kinds & 1) && n > 0) {
     constexpr int U = 4;
-    float4 cur[U];
+    auto cell = [&](const float4& A, int c) {
+      float pr = 0.f, acc = 0.f, E = 0.f;
+      if (!skip32) predict32(x, A, A.w, pr, acc, E);
+      if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
+      else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
+    };
+    int c0 = lane;
+    float4 a[U], b[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) cur[u] = sA[min(lane + u * W, n - 1)];
-    for (int c0 = lane; c0 < n; c0 += U * W) {
-      float4 nxt[U];
+    for (int u = 0; u < U; ++u) a[u] = sA[c0 + u * W];
+    for (; c0 + (2 * U - 1) * W < n; c0 += 2 * U * W) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) nxt[u] = sA[min(c0 + (U + u) * W, n - 1)];
+      for (int u = 0; u < U; ++u) b[u] = sA[c0 + (U + u) * W];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + u * W;
-        if (c < n) {
-          float pr = 0.f, acc = 0.f, E = 0.f;
-          if (!skip32) predict32(x, cur[u], cur[u].w, pr, acc, E);
-          if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
-          else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
-        }
-      }
+      for (int u = 0; u < U; ++u) cell(a[u], c0 + u * W);
 #pragma unroll
-      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+      for (int u = 0; u < U; ++u) a[u] = sA[c0 + (2 * U + u) * W];
+#pragma unroll
+      for (int u = 0; u < U; ++u) cell(b[u], c0 + (U + u) * W);
     }
+    for (int c = c0; c < n; c += W) cell(sA[c], c);
   }
   // Anytime columns: consecutive stages; the next stage row and the next
   // column descriptor are prefetched one step ahead.
@@ -438,12 +448,12 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
   if ((kinds & 2) && lane < ncol) {
     int2 cd = sCol[lane];
     for (int col = lane; col < ncol; col += W) {
-      const int2 cd_next = sCol[min(col + W, ncol - 1)];
+      const int2 cd_next = sCol[col + W];  // sCol is padded too
       float4 A = sA[cd.x];
       float acc = A.w;
       for (int k = 0; k < cd.y; ++k) {
         const int c = cd.x + k;
-        const float4 A_next = sA[cd.x + min(k + 1, cd.y - 1)];
+        const float4 A_next = sA[c + 1];  // padded table: always in bounds
         float pr = 0.f, E = 0.f;
         if (!skip32) predict32(x, A, acc, pr, acc, E);
         if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
@@ -453,6 +463,35 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
       cd = cd_next;
     }
   }
+}
+
+// Re-rank pass from the stored FP32 objectives (no re-scan): the same
+// cell-to-lane assignment as cell_pass, so each lane reads what it wrote.
+template <int MODE, bool HAS_PR, class Tile>
+__device__ __forceinline__ void refine_stored(const DevTable& T, const float4* __restrict__ sB,
+                                              const int2* __restrict__ sCol, const Tile& tile, const StepCtx& x,
+                                              int kinds, AlertScan<MODE, HAS_PR>& S) {
+  const int W = Tile::num_threads();
+  const int lane = tile.thread_rank();
+  const int L = S.level;
+  // packing perturbs the stored value by <= 3 ulp: widen the cut accordingly
+  const float cut = S.cut + fabsf(S.cut) * 4.8e-7f + 1e-30f;
+  auto check = [&](int c) {
+    const unsigned u = __float_as_uint(x.sv[c]);
+    const bool poss = L == 2 || ((u >> L) & 1u);
+    if (!S.all && !(poss && __uint_as_float(u) <= cut)) return;
+    Pred64 q = eval64(T, x, c);
+    if (!feasible64(x, q, L)) return;
+    Key64 k = key64(x, q, L, __float_as_uint(sB[c].y), c);
+    if (S.best.cell < 0 || k.less(S.best)) S.best = k;
+  };
+  if (kinds & 1)
+    for (int c = lane; c < T.n_trad; c += W) check(c);
+  if (kinds & 2)
+    for (int col = lane; col < T.n_any_cols; col += W) {
+      const int2 cd = sCol[col];
+      for (int k = 0; k < cd.y; ++k) check(cd.x + k);
+    }
 }
 
 // AlertPolicy.decide (policies.py:97-103) for the tile's stream.
@@ -518,7 +557,12 @@ __device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const fl
       S.all = x.fp64_all || (L == 2 && !(S.t[2].b1 < kInfF));  // level 2 never scanned: all relevant
       S.cut = S.all ? kInfF : cutoff<MODE>(x, L, S.t[L].b1);
       S.best.init();
-      cell_pass<1, TRACK_CONSTRAINED>(T, sA, sB, sCol, tile, x, kinds, S);
+      // stored objectives cover levels 0/1 and, for max-accuracy, level 2
+      // (same objective); min-energy level 2 (-acc) needs the re-scan
+      if (x.sv && !x.fp64_all && (MODE == ALERT_MODE_MAX_ACCURACY || L != 2))
+        refine_stored(T, sB, sCol, tile, x, kinds, S);
+      else
+        cell_pass<1, TRACK_CONSTRAINED>(T, sA, sB, sCol, tile, x, kinds, S);
       S.best.merge(tile);
       if (S.best.cell >= 0) {
         d.cell = S.best.cell;

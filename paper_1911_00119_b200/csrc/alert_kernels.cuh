@@ -25,7 +25,7 @@ struct RunParams {
   int policy;
   unsigned flags;
   int kinds;
-  int spec_smem, c64_smem, ratio_smem;  // staging decisions (host computed)
+  int spec_smem, c64_smem, ratio_smem, sv_smem;  // staging decisions (host computed)
   long long stream_begin, stream_end, step_begin, step_end;
   // Idle-filter gains (estimator.py:123-125) do not depend on the data: the
   // sequence M_k (state after k updates from m0) and W_k reaches an exact FP64
@@ -38,17 +38,18 @@ struct RunParams {
 
 // Shared-memory layout of run_kernel (host and device compute it identically).
 struct SmemLayout {
-  size_t B, col, spec, c64, ratio, agg, total;
+  size_t B, col, spec, c64, ratio, agg, sv, total;
   __host__ __device__ static size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
   __host__ __device__ SmemLayout(int n_cells, int n_cols, int n_spec, int n_c64, int n_tiles, int n_ratio,
-                                 size_t agg_bytes) {
-    B = sizeof(float4) * (size_t)n_cells;
+                                 size_t agg_bytes, int n_sv = 0) {
+    B = sizeof(float4) * (size_t)(n_cells + ALERT_SMEM_PAD);
     col = B + sizeof(float4) * (size_t)n_cells;
-    spec = up16(col + sizeof(int2) * (size_t)(n_cols + 1));
+    spec = up16(col + sizeof(int2) * (size_t)(n_cols + ALERT_SMEM_PAD));
     c64 = up16(spec + sizeof(SpecDev) * (size_t)n_spec);
     ratio = up16(c64 + sizeof(Cell64) * (size_t)n_c64);
     agg = up16(ratio + sizeof(double) * (size_t)n_tiles * (size_t)n_ratio);
-    total = up16(agg + agg_bytes * (size_t)n_tiles);
+    sv = up16(agg + agg_bytes * (size_t)n_tiles);
+    total = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);
   }
 };
 
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   const DevTable& T = P.T;
   const int n_tiles = blockDim.x / W;
   const SmemLayout L(T.n_cells, T.n_any_cols, P.spec_smem ? P.n_specs : 0, P.c64_smem ? T.n_cells : 0, n_tiles,
-                     P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg));
+                     P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
   float4* sB = reinterpret_cast<float4*>(base + L.B);
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   Cell64* sC64 = reinterpret_cast<Cell64*>(base + L.c64);
   double* sRatio = reinterpret_cast<double*>(base + L.ratio);
   TileAgg* sAgg = reinterpret_cast<TileAgg*>(base + L.agg);
+  float* sV = reinterpret_cast<float*>(base + L.sv);
   load_table_smem(T, sA, sB, sCol);
   if (P.spec_smem)
     for (int i = threadIdx.x; i < P.n_specs; i += blockDim.x) sSpec[i] = P.specs[i];
@@ -150,6 +152,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   const bool writer = tile.thread_rank() == 0;
   TileAgg& G = sAgg[threadIdx.x / W];
   double* ratio_tab = P.ratio_smem ? sRatio + (size_t)(threadIdx.x / W) * T.n_powers : nullptr;
+  float* sv_tile = P.sv_smem ? sV + (size_t)(threadIdx.x / W) * T.n_cells : nullptr;
 
   const int si = P.stream_spec ? P.stream_spec[stream] : (int)(stream % P.n_specs);
   const SpecDev* spec = P.spec_smem ? sSpec + si : P.specs + si;
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
     } else {
       StepCtx x;
       make_ctx(x, spec, C64, f.mu, f.sigma2, f.phi, goal, fp64_all);
+      x.sv = sv_tile;
       d = alert_decide(T, sA, sB, sCol, tile, x, kinds, no_refine);
       s = s_of_raw(tr, s_raw);
     }
@@ -351,9 +355,11 @@ template <int W>
 __global__ void __launch_bounds__(256) decide_kernel(const StepParams P, uint32_t* decision) {
   extern __shared__ float4 smem[];
   const DevTable& T = P.T;
+  const SmemLayout L(T.n_cells, T.n_any_cols, 0, 0, 0, 0, 0);
+  char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
-  float4* sB = smem + T.n_cells;
-  int2* sCol = reinterpret_cast<int2*>(sB + T.n_cells);
+  float4* sB = reinterpret_cast<float4*>(base + L.B);
+  int2* sCol = reinterpret_cast<int2*>(base + L.col);
   load_table_smem(T, sA, sB, sCol);
   __syncthreads();
   auto tile = cg::tiled_partition<W>(cg::this_thread_block());
