@@ -395,31 +395,38 @@ static int kinds_of(int policy, const AlertTable* tb) {
   return (k & have) ? k : 0;
 }
 
-static size_t table_smem(const AlertTable* tb) {
-  return SmemLayout(tb->dev.n_cells, tb->dev.n_any_cols, 0, 0, 0, 0, 0).total;
+static size_t table_smem(const AlertTable* tb, int W) {
+  return SmemLayout(tb->dev.n_cells, tb->dev.n_any_cols, 0, 0, 0, 0, 0, 0, W).total;
 }
 
 // Staging decisions of run_kernel: specs, FP64 cells and the per-segment
 // idle-ratio table go to shared memory when small (see SmemLayout).
-static void run_staging(const AlertTable* tb, int n_specs, int tpb, int W, RunParams& P) {
+static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_specs, int tpb, int W, RunParams& P) {
   const DevTable& T = tb->dev;
   P.spec_smem = n_specs <= kSpecSmemMax;
   P.c64_smem = T.n_cells <= kC64SmemMax;
   P.ratio_smem = T.n_powers <= kRatioSmemMax &&
                  (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;
-  P.sv_smem = (size_t)(tpb / W) * (size_t)T.n_cells * sizeof(float) <= 32 * 1024;
+  // stored objectives pay off only where FP64 re-ranks are frequent:
+  // max-accuracy with a completion-probability threshold (SURVEY §7 hard part 1)
+  bool refine_heavy = false;
+  for (int k = 0; k < n_specs; ++k)
+    refine_heavy |= specs[k].mode == ALERT_MODE_MAX_ACCURACY && specs[k].has_pr;
+  P.sv_smem = refine_heavy && (size_t)(tpb / W) * (size_t)T.n_cells * sizeof(float) <= 32 * 1024;
 }
 
 static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const RunParams& P) {
   const DevTable& T = tb->dev;
   SmemLayout L(T.n_cells, T.n_any_cols, P.spec_smem ? n_specs : 0, P.c64_smem ? T.n_cells : 0, tpb / W,
-               P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0);
+               P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W);
   return L.total;
 }
 
 static int pick_lanes(const AlertContext* ctx, const AlertTable* tb) {
   if (ctx->lanes) return ctx->lanes;
-  return tb->n_cand <= 256 ? 1 : 32;
+  // measured on B200 (profiles/): one lane per stream for small tables (no
+  // redundant per-step work), 4-lane tiles for the 2,144-candidate table
+  return tb->n_cand <= 256 ? 1 : 4;
 }
 
 // Upload host specs to stream-ordered device memory (freed after the launch).
@@ -540,7 +547,7 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   if (stream_end == stream_begin || step_end == step_begin) return ALERT_OK;
   int W = pick_lanes(ctx, tb);
   RunParams P;
-  run_staging(tb, n_specs, ctx->tpb, W, P);
+  run_staging(tb, specs, n_specs, ctx->tpb, W, P);
   size_t smem = run_smem(tb, n_specs, ctx->tpb, W, P);
   if ((int)smem > ctx->max_smem) return fail(ALERT_ERR_UNSUPPORTED, "alert_run: table exceeds shared memory");
   idle_table(*cfg, P);
@@ -583,7 +590,7 @@ int alert_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs
   int kinds = kinds_of(policy, tb);
   if (!kinds) return fail(ALERT_ERR_NO_CANDIDATE, "alert_decide: space has no DNN of the policy's kinds");
   if (n <= 0) return n < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_decide: n < 0") : ALERT_OK;
-  size_t smem = table_smem(tb);
+  size_t smem = table_smem(tb, pick_lanes(ctx, tb));
   if ((int)smem > ctx->max_smem) return fail(ALERT_ERR_UNSUPPORTED, "alert_decide: table exceeds shared memory");
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;

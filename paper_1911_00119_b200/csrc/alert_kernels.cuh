@@ -40,11 +40,14 @@ struct RunParams {
 struct SmemLayout {
   size_t B, col, spec, c64, ratio, agg, sv, total;
   __host__ __device__ static size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
+  // pad = look-ahead rows past the end of the cell / column tables for a tile
+  // width W: 2 chunks of 4 cells (see cell_pass), so 8 W + 8.
+  __host__ __device__ static int pad_rows(int W) { return 8 * W + 8; }
   __host__ __device__ SmemLayout(int n_cells, int n_cols, int n_spec, int n_c64, int n_tiles, int n_ratio,
-                                 size_t agg_bytes, int n_sv = 0) {
-    B = sizeof(float4) * (size_t)(n_cells + ALERT_SMEM_PAD);
+                                 size_t agg_bytes, int n_sv, int W) {
+    B = sizeof(float4) * (size_t)(n_cells + pad_rows(W));
     col = B + sizeof(float4) * (size_t)n_cells;
-    spec = up16(col + sizeof(int2) * (size_t)(n_cols + ALERT_SMEM_PAD));
+    spec = up16(col + sizeof(int2) * (size_t)(n_cols + pad_rows(W)));
     c64 = up16(spec + sizeof(SpecDev) * (size_t)n_spec);
     ratio = up16(c64 + sizeof(Cell64) * (size_t)n_c64);
     agg = up16(ratio + sizeof(double) * (size_t)n_tiles * (size_t)n_ratio);
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   const DevTable& T = P.T;
   const int n_tiles = blockDim.x / W;
   const SmemLayout L(T.n_cells, T.n_any_cols, P.spec_smem ? P.n_specs : 0, P.c64_smem ? T.n_cells : 0, n_tiles,
-                     P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0);
+                     P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
   float4* sB = reinterpret_cast<float4*>(base + L.B);
@@ -355,7 +358,7 @@ template <int W>
 __global__ void __launch_bounds__(256) decide_kernel(const StepParams P, uint32_t* decision) {
   extern __shared__ float4 smem[];
   const DevTable& T = P.T;
-  const SmemLayout L(T.n_cells, T.n_any_cols, 0, 0, 0, 0, 0);
+  const SmemLayout L(T.n_cells, T.n_any_cols, 0, 0, 0, 0, 0, 0, W);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
   float4* sB = reinterpret_cast<float4*>(base + L.B);
