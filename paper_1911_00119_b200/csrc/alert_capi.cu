@@ -293,7 +293,11 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     double qf = d->dnn_q_fail[i];
     double prev = k0 == 0 ? qf : d->stage_accuracy[stage_off[i] + k0 - 1];
     uint32_t key = ((uint32_t)j << 20) | ((uint32_t)i << 8) | (uint32_t)st;
-    A[cell] = make_float4((float)(1.0 / t), (float)(d->power_cap[j] * t), (float)(a - prev), (float)qf);
+    // .w = base of the running expected accuracy: q_fail for a traditional cell
+    // or the first stage of an anytime column, -1 (= "carry the previous
+    // stage's value") for later stages
+    A[cell] = make_float4((float)(1.0 / t), (float)(d->power_cap[j] * t), (float)(a - prev),
+                          k0 == 0 ? (float)qf : -1.0f);
     float kb, cb, sb;
     memcpy(&kb, &key, 4);
     memcpy(&cb, &cand, 4);
@@ -403,7 +407,6 @@ static size_t table_smem(const AlertTable* tb, int W) {
 // idle-ratio table go to shared memory when small (see SmemLayout).
 static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_specs, int tpb, int W, RunParams& P) {
   const DevTable& T = tb->dev;
-  P.spec_smem = n_specs <= kSpecSmemMax;
   P.c64_smem = T.n_cells <= kC64SmemMax;
   P.ratio_smem = T.n_powers <= kRatioSmemMax &&
                  (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;
@@ -417,7 +420,7 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
 
 static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const RunParams& P) {
   const DevTable& T = tb->dev;
-  SmemLayout L(T.n_cells, T.n_any_cols, P.spec_smem ? n_specs : 0, P.c64_smem ? T.n_cells : 0, tpb / W,
+  SmemLayout L(T.n_cells, T.n_any_cols, tpb / W, P.c64_smem ? T.n_cells : 0, tpb / W,
                P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W);
   return L.total;
 }

@@ -144,7 +144,8 @@ struct StepCtx {
   // thresholds with margins
   float q_hi, q_lo, th_hi, th_lo, e_hi, e_lo;
   bool fp64_all;
-  float* sv;  // per-tile FP32 objective of every cell (shared memory) or nullptr
+  unsigned sv;   // shared-space address of the tile's per-cell FP32 objectives
+  bool has_sv;   // stored objectives enabled
 };
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -159,7 +160,8 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
                                          double sigma2, double phi, double goal, bool fp64_all) {
   x.spec = sp;
   x.c64 = c64;
-  x.sv = nullptr;
+  x.sv = 0;
+  x.has_sv = false;
   x.mu = mu;
   x.sig = sigma2;  // holds sigma2 until ensure_fp64()
   x.phi = phi;
@@ -367,7 +369,9 @@ struct AlertScan {
     // keep the level-0 objective (min-energy: E; max-accuracy: -acc, the same
     // for every level) with the "possible" bits of levels 0/1 in its two low
     // mantissa bits, for the re-rank pass
-    if (x.sv) x.sv[c] = __uint_as_float((__float_as_uint(v) & ~3u) | (unsigned)p | ((unsigned)p1 << 1));
+    if (x.has_sv)
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(x.sv + 4u * c),
+                   "r"((__float_as_uint(v) & ~3u) | (unsigned)p | ((unsigned)p1 << 1)));
   }
 
   __device__ __forceinline__ void refine_cell(const DevTable& T, const StepCtx& x, int c, float pr,
@@ -417,12 +421,19 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
   // without register copies; the shared table is padded by ALERT_SMEM_PAD rows
   // so look-ahead loads need no clamping.  Full double chunks first, then the
   // remainder one cell at a time.
-  const int n = T.n_trad;
+  // One lane per stream (W = 1) with every kind admitted: ALL cells in one
+  // flat loop; an anytime stage continues the running accuracy of the previous
+  // cell (A.w < 0 marks "carry"), so columns need no inner loop.
+  const bool flat = W == 1 && kinds == 3;
+  const int n = flat ? T.n_cells : T.n_trad;
   if ((kinds & 1) && n > 0) {
     constexpr int U = 4;
+    float carry = 0.f;
     auto cell = [&](const float4& A, int c) {
       float pr = 0.f, acc = 0.f, E = 0.f;
-      if (!skip32) predict32(x, A, A.w, pr, acc, E);
+      const float base = A.w >= 0.0f ? A.w : carry;
+      if (!skip32) predict32(x, A, base, pr, acc, E);
+      carry = acc;
       if (PASS == 0) S.template scan_cell<TRACK>(x, c, pr, acc, E);
       else S.refine_cell(T, x, c, pr, acc, E, __float_as_uint(sB[c].y));
     };
@@ -445,7 +456,7 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
   // Anytime columns: consecutive stages; the next stage row and the next
   // column descriptor are prefetched one step ahead.
   const int ncol = T.n_any_cols;
-  if ((kinds & 2) && lane < ncol) {
+  if (!flat && (kinds & 2) && lane < ncol) {
     int2 cd = sCol[lane];
     for (int col = lane; col < ncol; col += W) {
       const int2 cd_next = sCol[col + W];  // sCol is padded too
@@ -477,7 +488,8 @@ __device__ __forceinline__ void refine_stored(const DevTable& T, const float4* _
   // packing perturbs the stored value by <= 3 ulp: widen the cut accordingly
   const float cut = S.cut + fabsf(S.cut) * 4.8e-7f + 1e-30f;
   auto check = [&](int c) {
-    const unsigned u = __float_as_uint(x.sv[c]);
+    unsigned u;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(u) : "r"(x.sv + 4u * c));
     const bool poss = L == 2 || ((u >> L) & 1u);
     if (!S.all && !(poss && __uint_as_float(u) <= cut)) return;
     Pred64 q = eval64(T, x, c);
@@ -559,7 +571,7 @@ __device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const fl
       S.best.init();
       // stored objectives cover levels 0/1 and, for max-accuracy, level 2
       // (same objective); min-energy level 2 (-acc) needs the re-scan
-      if (x.sv && !x.fp64_all && (MODE == ALERT_MODE_MAX_ACCURACY || L != 2))
+      if (x.has_sv && !x.fp64_all && (MODE == ALERT_MODE_MAX_ACCURACY || L != 2))
         refine_stored(T, sB, sCol, tile, x, kinds, S);
       else
         cell_pass<1, TRACK_CONSTRAINED>(T, sA, sB, sCol, tile, x, kinds, S);

@@ -25,7 +25,7 @@ struct RunParams {
   int policy;
   unsigned flags;
   int kinds;
-  int spec_smem, c64_smem, ratio_smem, sv_smem;  // staging decisions (host computed)
+  int c64_smem, ratio_smem, sv_smem;  // staging decisions (host computed)
   long long stream_begin, stream_end, step_begin, step_end;
   // Idle-filter gains (estimator.py:123-125) do not depend on the data: the
   // sequence M_k (state after k updates from m0) and W_k reaches an exact FP64
@@ -38,7 +38,7 @@ struct RunParams {
 
 // Shared-memory layout of run_kernel (host and device compute it identically).
 struct SmemLayout {
-  size_t B, col, spec, c64, ratio, agg, sv, total;
+  size_t B, col, spec, c64, ratio, agg, sv, slot, total;
   __host__ __device__ static size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
   // pad = look-ahead rows past the end of the cell / column tables for a tile
   // width W: 2 chunks of 4 cells (see cell_pass), so 8 W + 8.
@@ -52,7 +52,8 @@ struct SmemLayout {
     ratio = up16(c64 + sizeof(Cell64) * (size_t)n_c64);
     agg = up16(ratio + sizeof(double) * (size_t)n_tiles * (size_t)n_ratio);
     sv = up16(agg + agg_bytes * (size_t)n_tiles);
-    total = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);
+    slot = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);
+    total = up16(slot + 16 * (size_t)n_tiles * (size_t)W);  // two 8-byte trace slots per thread
   }
 };
 
@@ -75,6 +76,15 @@ __device__ __forceinline__ unsigned long long load_s_raw(const AlertTrace& tr, l
 __device__ __forceinline__ double s_of_raw(const AlertTrace& tr, unsigned long long raw) {
   return tr.slowdown_dtype == ALERT_DTYPE_F64 ? __longlong_as_double((long long)raw)
                                               : (double)__uint_as_float((unsigned int)raw);
+}
+
+__device__ __forceinline__ void prefetch_s(unsigned dst, const char* src, bool f64) {
+  if (f64)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\ncp.async.commit_group;\n" ::"r"(dst), "l"(src)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\ncp.async.commit_group;\n" ::"r"(dst), "l"(src)
+                 : "memory");
 }
 
 // Per-tile accumulators in shared memory (touched once per step by the tile's
@@ -130,7 +140,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   extern __shared__ float4 smem[];
   const DevTable& T = P.T;
   const int n_tiles = blockDim.x / W;
-  const SmemLayout L(T.n_cells, T.n_any_cols, P.spec_smem ? P.n_specs : 0, P.c64_smem ? T.n_cells : 0, n_tiles,
+  const SmemLayout L(T.n_cells, T.n_any_cols, n_tiles, P.c64_smem ? T.n_cells : 0, n_tiles,
                      P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
@@ -142,8 +152,6 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   TileAgg* sAgg = reinterpret_cast<TileAgg*>(base + L.agg);
   float* sV = reinterpret_cast<float*>(base + L.sv);
   load_table_smem(T, sA, sB, sCol);
-  if (P.spec_smem)
-    for (int i = threadIdx.x; i < P.n_specs; i += blockDim.x) sSpec[i] = P.specs[i];
   if (P.c64_smem)
     for (int i = threadIdx.x; i < T.n_cells; i += blockDim.x) sC64[i] = T.c64[i];
   __syncthreads();
@@ -155,10 +163,18 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   const bool writer = tile.thread_rank() == 0;
   TileAgg& G = sAgg[threadIdx.x / W];
   double* ratio_tab = P.ratio_smem ? sRatio + (size_t)(threadIdx.x / W) * T.n_powers : nullptr;
-  float* sv_tile = P.sv_smem ? sV + (size_t)(threadIdx.x / W) * T.n_cells : nullptr;
+  const unsigned sv_tile = (unsigned)__cvta_generic_to_shared(sV + (size_t)(threadIdx.x / W) * T.n_cells);
 
   const int si = P.stream_spec ? P.stream_spec[stream] : (int)(stream % P.n_specs);
-  const SpecDev* spec = P.spec_smem ? sSpec + si : P.specs + si;
+  // the stream's spec, copied once into the tile's shared slot (all per-step
+  // spec reads are then shared-memory loads)
+  SpecDev* spec = sSpec + threadIdx.x / W;
+  {
+    const float4* src = reinterpret_cast<const float4*>(P.specs + si);
+    float4* dst = reinterpret_cast<float4*>(spec);
+    for (int k = tile.thread_rank(); k < (int)(sizeof(SpecDev) / 16); k += W) dst[k] = src[k];
+    tile.sync();
+  }
   const AlertTrace& tr = P.tr;
   const long long row = tr.stream_row ? tr.stream_row[stream] : stream;
 
@@ -181,14 +197,12 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
 
   // segment (phase) tracking
   const int nseg = tr.n_segments[row];
-  const int32_t* seg_end = tr.seg_end + row * tr.max_segments;
-  const int32_t* seg_phase = tr.seg_phase + row * tr.max_segments;
-  const double* seg_idle = tr.seg_idle + row * tr.max_segments;
+  const long long seg0 = row * tr.max_segments;  // segment arrays are re-read only at segment changes
   int seg = 0;
-  while (seg + 1 < nseg && P.step_begin >= seg_end[seg]) ++seg;
-  int cur_end = seg_end[seg];
-  int phase = seg_phase[seg];
-  double idle = seg_idle[seg];
+  while (seg + 1 < nseg && P.step_begin >= tr.seg_end[seg0 + seg]) ++seg;
+  int cur_end = tr.seg_end[seg0 + seg];
+  int phase = tr.seg_phase[seg0 + seg];
+  double idle = tr.seg_idle[seg0 + seg];
   if (ratio_tab) fill_ratios(T, tile, ratio_tab, idle);
 
   double* agg = P.out.agg ? P.out.agg + stream * ALERT_AGG_FIELDS : nullptr;
@@ -208,18 +222,34 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   const bool no_refine = P.flags & ALERT_FLAG_NO_REFINE;
   const int* forced = P.out.forced;
 
-  unsigned long long s_next = load_s_raw(tr, row, P.step_begin);
-  for (long long n = P.step_begin; n < P.step_end; ++n) {
-    const unsigned long long s_raw = s_next;
-    if (n + 1 < P.step_end) s_next = load_s_raw(tr, row, n + 1);
+  // Trace prefetch: the next step's slow-down is copied global -> shared with
+  // cp.async (LDGSTS) into one of two per-thread slots, so no register is held
+  // across the step and the load latency hides behind a whole step of work.
+  unsigned long long* slot = reinterpret_cast<unsigned long long*>(base + L.slot) + 2 * threadIdx.x;
+  const unsigned slot_sa = (unsigned)__cvta_generic_to_shared(slot);
+  const bool f64 = tr.slowdown_dtype == ALERT_DTYPE_F64;
+  const int esz = f64 ? 8 : 4;
+  const char* sptr = static_cast<const char*>(tr.slowdown) +
+                     (row * tr.row_stride + (P.step_begin - tr.step_offset) * tr.step_stride) * esz;
+  const long long sinc = tr.step_stride * esz;
+  prefetch_s(slot_sa, sptr, f64);
+  const int nsteps = (int)(P.step_end - P.step_begin);
+  for (int i = 0; i < nsteps; ++i) {
+    const long long n = P.step_begin + i;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    const unsigned long long s_raw = slot[i & 1];
+    if (i + 1 < nsteps) {
+      sptr += sinc;
+      prefetch_s(slot_sa + 8u * ((i + 1) & 1), sptr, f64);
+    }
     if (n >= cur_end && seg + 1 < nseg) {
       if (agg && writer) flush_segment(G, agg, phase);
       while (seg + 1 < nseg && n >= cur_end) {
         ++seg;
-        cur_end = seg_end[seg];
+        cur_end = tr.seg_end[seg0 + seg];
       }
-      phase = seg_phase[seg];
-      idle = seg_idle[seg];
+      phase = tr.seg_phase[seg0 + seg];
+      idle = tr.seg_idle[seg0 + seg];
       if (ratio_tab) fill_ratios(T, tile, ratio_tab, idle);
       if (agg && writer) open_segment(G, agg, phase);
     }
@@ -247,6 +277,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
       StepCtx x;
       make_ctx(x, spec, C64, f.mu, f.sigma2, f.phi, goal, fp64_all);
       x.sv = sv_tile;
+      x.has_sv = P.sv_smem;
       d = alert_decide(T, sA, sB, sCol, tile, x, kinds, no_refine);
       s = s_of_raw(tr, s_raw);
     }
