@@ -117,7 +117,9 @@ __device__ __forceinline__ float phi32_x(float x) {
   const float al = a * 1.44269504088896341f;
   const float e = ex2_approx(fmaf(-al, a, -1.0f));  // e^{-a^2} / 2
   const float h = (p * t) * e;                      // erfc(a) / 2
-  return x >= 0.0f ? 1.0f - h : h;
+  // Phi = 1/2 + sign(x) (1/2 - h): copysign is one LOP3, the rest FMA-pipe work
+  const float half_sgn = __uint_as_float((__float_as_uint(x) & 0x80000000u) | 0x3f000000u);
+  return fmaf(half_sgn, fmaf(-2.0f, h, 1.0f), 0.5f);
 }
 
 // deadline_probability, exact reference arithmetic (predictor.py:48-65).
@@ -369,7 +371,8 @@ struct AlertScan {
     // keep the level-0 objective (min-energy: E; max-accuracy: -acc, the same
     // for every level) with the "possible" bits of levels 0/1 in its two low
     // mantissa bits, for the re-rank pass
-    if (x.has_sv)
+    // only the refine-heavy variant (max-accuracy with pr_threshold) stores
+    if (MODE == ALERT_MODE_MAX_ACCURACY && HAS_PR && x.has_sv)
       asm volatile("st.shared.u32 [%0], %1;" ::"r"(x.sv + 4u * c),
                    "r"((__float_as_uint(v) & ~3u) | (unsigned)p | ((unsigned)p1 << 1)));
   }
@@ -451,7 +454,13 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
 #pragma unroll
       for (int u = 0; u < U; ++u) cell(b[u], c0 + (U + u) * W);
     }
-    for (int c = c0; c < n; c += W) cell(sA[c], c);
+    // tail (< 2U cells): a[] already holds the next U rows
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + u * W < n) cell(a[u], c0 + u * W);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (c0 + (U + u) * W < n) cell(sA[c0 + (U + u) * W], c0 + (U + u) * W);
   }
   // Anytime columns: consecutive stages; the next stage row and the next
   // column descriptor are prefetched one step ahead.
@@ -571,7 +580,7 @@ __device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const fl
       S.best.init();
       // stored objectives cover levels 0/1 and, for max-accuracy, level 2
       // (same objective); min-energy level 2 (-acc) needs the re-scan
-      if (x.has_sv && !x.fp64_all && (MODE == ALERT_MODE_MAX_ACCURACY || L != 2))
+      if (MODE == ALERT_MODE_MAX_ACCURACY && HAS_PR && x.has_sv && !x.fp64_all)
         refine_stored(T, sB, sCol, tile, x, kinds, S);
       else
         cell_pass<1, TRACK_CONSTRAINED>(T, sA, sB, sCol, tile, x, kinds, S);
