@@ -352,7 +352,9 @@ def main():
         quality["oracle_mean_accuracy"] = float((tot[abi.AGG_OR_ACC] + tot[abi.AGG_OR_ACC_C]) / n_all)
 
     # roofline of the dominant kernel (run_kernel): algorithmic FP32 slots per decision
-    slots = 30 * C + 60
+    # ALERT 30 C + 60 FP32 slots and C + 6 MUFU per decision;
+    # the oracle evaluated alongside (config 5) adds 15 C + 20 slots, no MUFU
+    slots = 30 * C + 60 + (15 * C + 20 if policy == "alert+oracle" else 0)
     mufu = C + 6
     per_launch = S * N
     ach = per_launch * slots / (kernel_ms * 1e-3)

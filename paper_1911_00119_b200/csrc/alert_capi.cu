@@ -44,6 +44,7 @@ struct AlertTable {
   void* buf = nullptr;  // one device allocation holding every array
   int n_cand = 0;
   std::vector<int32_t> cand_dnn, cand_power, cand_stage;
+  std::vector<double> acc_levels;  // distinct accuracies, descending (rank order)
   int n_any_cols = 0;
   int device = 0;
 };
@@ -268,7 +269,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
       }
     }
   const int n = c;
-  if (n > ALERT_MAX_CANDIDATES || P > 1023 || d->n_dnns > 4095) {
+  if (n > ALERT_MAX_CANDIDATES || P > 1023 || d->n_dnns > 4095 || d->n_dnns * (ALERT_MAX_STAGES + 1) > 65535) {
     delete tb;
     return fail(ALERT_ERR_UNSUPPORTED, "table too large for the packed tie-break key / shared memory");
   }
@@ -280,6 +281,20 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     for (int k = 0; k < ns; ++k) order.push_back(any_cells[q + k]);
     q += ns;
   }
+  // exact accuracy classes: every distinct stage accuracy / q_fail value,
+  // descending; rank 0 = most accurate (oracle FP32 scan compares ranks)
+  std::vector<double> levels;
+  for (int i = 0; i < d->n_dnns; ++i) {
+    levels.push_back(d->dnn_q_fail[i]);
+    for (int k = 0; k < d->dnn_n_stages[i]; ++k) levels.push_back(d->stage_accuracy[stage_off[i] + k]);
+  }
+  std::sort(levels.begin(), levels.end(), [](double x, double y) { return x > y; });
+  levels.erase(std::unique(levels.begin(), levels.end()), levels.end());
+  auto rank_of = [&](double v) {
+    return (uint32_t)(std::lower_bound(levels.begin(), levels.end(), v, [](double x, double y) { return x > y; }) -
+                      levels.begin());
+  };
+  tb->acc_levels = levels;
   std::vector<float4> A(n), B(n);
   std::vector<Cell64> c64(n);
   std::vector<int> cell_of_cand(n);
@@ -298,11 +313,14 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     // stage's value") for later stages
     A[cell] = make_float4((float)(1.0 / t), (float)(d->power_cap[j] * t), (float)(a - prev),
                           k0 == 0 ? (float)qf : -1.0f);
-    float kb, cb, sb;
+    // .z = candidate | stage << 16; .w = rank(stage accuracy) | rank(q_fail) << 16
+    const uint32_t cs = (uint32_t)cand | ((uint32_t)st << 16);
+    const uint32_t rk = rank_of(a) | (rank_of(qf) << 16);
+    float kb, cb, rb;
     memcpy(&kb, &key, 4);
-    memcpy(&cb, &cand, 4);
-    memcpy(&sb, &st, 4);
-    B[cell] = make_float4((float)t, kb, cb, sb);
+    memcpy(&cb, &cs, 4);
+    memcpy(&rb, &rk, 4);
+    B[cell] = make_float4((float)t, kb, cb, rb);
     c64[cell] = Cell64{t, a, qf, d->power_cap[j]};
     cell_of_cand[cand] = cell;
   }
@@ -344,6 +362,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   double r = d->p_idle_prof / max_cap;
   T.phi0 = (1.0 < r) ? 1.0 : r;  // min(1.0, p_idle_prof / max cap), policies.py:90
   T.power_cap64 = reinterpret_cast<const double*>(buf + oPw);
+  T.cap_max = (float)max_cap;
   tb->buf = buf;
   tb->n_cand = n;
   tb->n_any_cols = (int)cols.size();
@@ -436,7 +455,7 @@ static int pick_lanes(const AlertContext* ctx, const AlertTable* tb) {
 // AlertSpec -> SpecDev (device form): goal0 / period0 with the reference's
 // operations (selector.py:48-70: max(t_goal - overhead, 0.001); simulator.py:483),
 // FP32 copies for the scan.
-static SpecDev spec_dev(const AlertSpec& a) {
+static SpecDev spec_dev(const AlertSpec& a, const AlertTable* tb) {
   SpecDev d{};
   d.t_goal = a.t_goal;
   d.e_goal = a.e_goal;
@@ -455,13 +474,17 @@ static SpecDev spec_dev(const AlertSpec& a) {
   d.mode = a.mode;
   d.has_pr = a.has_pr;
   d.group_size = a.group_size;
+  // delivered >= q_goal  <=>  rank(delivered) < rank_q  (ranks are descending)
+  int rq = 0;
+  while (rq < (int)tb->acc_levels.size() && tb->acc_levels[rq] >= a.q_goal) ++rq;
+  d.rank_q = rq;
   return d;
 }
 
 // Upload host specs to stream-ordered device memory (freed after the launch).
-static int upload_specs(const AlertSpec* specs, int n, cudaStream_t st, SpecDev** dev) {
+static int upload_specs(const AlertSpec* specs, int n, const AlertTable* tb, cudaStream_t st, SpecDev** dev) {
   std::vector<SpecDev> h(n);
-  for (int k = 0; k < n; ++k) h[k] = spec_dev(specs[k]);
+  for (int k = 0; k < n; ++k) h[k] = spec_dev(specs[k], tb);
   CUDA_TRY(cudaMallocAsync((void**)dev, sizeof(SpecDev) * n, st));
   CUDA_TRY(cudaMemcpyAsync(*dev, h.data(), sizeof(SpecDev) * n, cudaMemcpyHostToDevice, st));
   // pageable source: the copy is staged before cudaMemcpyAsync returns
@@ -557,7 +580,7 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   SpecDev* dspecs = nullptr;
-  r = upload_specs(specs, n_specs, s, &dspecs);
+  r = upload_specs(specs, n_specs, tb, s, &dspecs);
   if (r) return r;
   P.T = tb->dev;
   P.cfg = *cfg;
@@ -598,7 +621,7 @@ int alert_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   SpecDev* dspecs = nullptr;
-  r = upload_specs(specs, n_specs, s, &dspecs);
+  r = upload_specs(specs, n_specs, tb, s, &dspecs);
   if (r) return r;
   StepParams P{};
   P.T = tb->dev;
@@ -637,7 +660,7 @@ int alert_predict(AlertContext* ctx, const AlertTable* tb, const AlertSpec* spec
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   SpecDev* dspecs = nullptr;
-  r = upload_specs(specs, n_specs, s, &dspecs);
+  r = upload_specs(specs, n_specs, tb, s, &dspecs);
   if (r) return r;
   // per-candidate (dnn, power, stage) arrays in stream-ordered scratch
   int nc = tb->n_cand;
@@ -682,7 +705,6 @@ int alert_observe(AlertContext* ctx, const AlertTable* tb, const AlertFilterConf
 int alert_oracle_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs, int32_t n_specs,
                         const int32_t* stream_spec, const double* sd, const double* idle, const double* plan_goal,
                         uint32_t flags, uint32_t* decision, int64_t n, void* cuda_stream) {
-  (void)flags;
   if (!ctx || !tb || !sd || !idle || !plan_goal || !decision)
     return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_oracle_decide: NULL argument");
   int r = check_specs(specs, n_specs);
@@ -691,19 +713,19 @@ int alert_oracle_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = (cudaStream_t)cuda_stream;
   SpecDev* dspecs = nullptr;
-  r = upload_specs(specs, n_specs, s, &dspecs);
+  r = upload_specs(specs, n_specs, tb, s, &dspecs);
   if (r) return r;
   int W = pick_lanes(ctx, tb);
   int tpb = ctx->tpb;
   unsigned blocks = (unsigned)((n * W + tpb - 1) / tpb);
   cudaError_t e;
   switch (W) {
-    case 1: e = launch_oracle<1>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
-    case 2: e = launch_oracle<2>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
-    case 4: e = launch_oracle<4>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
-    case 8: e = launch_oracle<8>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
-    case 16: e = launch_oracle<16>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
-    default: e = launch_oracle<32>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, s); break;
+    case 1: e = launch_oracle<1>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
+    case 2: e = launch_oracle<2>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
+    case 4: e = launch_oracle<4>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
+    case 8: e = launch_oracle<8>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
+    case 16: e = launch_oracle<16>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
+    default: e = launch_oracle<32>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
   }
   cudaFreeAsync(dspecs, s);
   if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("oracle_decide_kernel: ") + cudaGetErrorString(e));

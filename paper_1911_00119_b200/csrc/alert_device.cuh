@@ -42,12 +42,13 @@ struct DevTable {
   int n_any_cols;   // anytime columns (dnn, power) after the traditional cells
   int n_powers;
   const float4* cellA;    // {1/t, cap*t, d = a_k - a_{k-1} (a_0 = q_fail), q_fail}   FP32 scan
-  const float4* cellB;    // {t, tie-key bits, candidate index bits, stage bits}   refine / decode
+  const float4* cellB;    // {t, tie-key, candidate | stage << 16, rank(acc) | rank(q_fail) << 16}
   const int2* any_cols;   // {first cell, number of stages}
   const struct Cell64* c64;  // FP64 cell data (exact path), AoS
   const int* cell_of_cand;
   const double* power_cap64;  // [n_powers] caps by power index
   double phi0;            // min(1, p_idle_prof / max cap), policies.py:90
+  float cap_max;          // largest cap (FP32 error bound of the oracle scan)
 };
 
 // FP64 data of one cell for the exact path: profiled latency of the cell's
@@ -63,8 +64,15 @@ struct Cell64 {
 struct SpecDev {
   double t_goal, e_goal, q_goal, pr_th, zq, oh, goal0, period0;
   float q_f, e_f, th_f, zq_f;
-  int mode, has_pr, group_size, pad;
+  int mode, has_pr, group_size;
+  int rank_q;  // delivered >= q_goal  <=>  accuracy rank < rank_q (oracle scan)
 };
+
+// cellB field accessors
+__device__ __forceinline__ int cell_cand(const float4& B) { return __float_as_uint(B.z) & 0xFFFF; }
+__device__ __forceinline__ int cell_stage(const float4& B) { return __float_as_uint(B.z) >> 16; }
+__device__ __forceinline__ int cell_rank_a(const float4& B) { return __float_as_uint(B.w) & 0xFFFF; }
+__device__ __forceinline__ int cell_rank_qf(const float4& B) { return __float_as_uint(B.w) >> 16; }
 
 // Exact FP64 helpers: no FMA contraction, Python's min/max semantics.
 __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
@@ -258,7 +266,7 @@ struct Pred64 {
 
 __device__ __forceinline__ Pred64 eval64(const DevTable& T, const StepCtx& x, int c) {
   Pred64 r;
-  const int stage = __float_as_int(T.cellB[c].w);  // 0 = traditional
+  const int stage = cell_stage(T.cellB[c]);  // 0 = traditional
   const Cell64* C = x.c64;
   double t = C[c].t;
   double qf = C[c].qf;
@@ -621,7 +629,7 @@ struct Outcome {
 __device__ __forceinline__ Outcome execute_measure(const float4* sB, const Cell64* C, const SpecDev* sp, int c,
                                                    double s, double goal, double period, double idle) {
   Outcome o;
-  const int stage = __float_as_int(sB[c].w);
+  const int stage = cell_stage(sB[c]);
   const int first = stage == 0 ? c : c - (stage - 1);
   double lat;
   if (stage == 0) {
@@ -706,7 +714,7 @@ __device__ __forceinline__ void idle_update(const AlertFilterConfig& cfg, Filter
 // OraclePolicy.decide (policies.py:160-205): exact per-cell outcome under the
 // true slow-down, three fallback levels at once, FP64.
 template <class Tile>
-__device__ Decision oracle_decide(const DevTable& T, const float4* sB, const Cell64* C, const int2* sCol,
+__device__ Decision oracle_decide_exact(const DevTable& T, const float4* sB, const Cell64* C, const int2* sCol,
                                   const Tile& tile, const SpecDev* sp, double s,
                                   double idle, double goal) {
   const int W = Tile::num_threads();
@@ -762,6 +770,298 @@ __device__ Decision oracle_decide(const DevTable& T, const float4* sB, const Cel
     if (d.cell < 0 && best[lvl].cell >= 0) { d.cell = best[lvl].cell; d.level = lvl; }
   }
   return d;
+}
+
+
+// --------------------------------------------------------------------------
+// OraclePolicy.decide with an FP32 scan (policies.py:160-205).  Per cell, in
+// FP32: completion under the true slow-down (x = s t vs the goal, with an
+// uncertainty band: "poison" when x is within a few ulp of the goal), the
+// delivered-accuracy CLASS (exact integer rank of the table value, see
+// alert_table_create) and the energy.  Max-delivered-accuracy levels use a
+// lexicographic (rank, energy) tracker, so exact accuracy ties between powers
+// of one DNN are resolved in FP32; min-energy levels use the energy tracker.
+// Anything not provably decided (energy within the FP32 bound, poisoned
+// completions) is re-ranked exactly in FP64 (execute_measure + the reference
+// keys).  ALERT_FLAG_FP64_ALL uses oracle_decide_exact throughout.
+struct LexTracker {
+  int r1, i1, un;   // best rank (sure), its cell, lowest possible rank among uncertain
+  float e1, e2;     // best / second-best energy inside class r1
+  __device__ __forceinline__ void init() { r1 = un = 0x7fffffff; i1 = -1; e1 = e2 = kInfF; }
+  __device__ __forceinline__ void push(int r, float e, bool sure, bool unc, int r_unc, int c) {
+    const bool lt = sure && r < r1, eq = sure && r == r1;
+    const bool nb = lt || (eq && e < e1);
+    e2 = lt ? kInfF : (eq ? fminf(e2, fmaxf(e1, e)) : e2);
+    e1 = lt ? e : (eq ? fminf(e1, e) : e1);
+    i1 = nb ? c : i1;
+    r1 = lt ? r : r1;
+    un = unc ? min(un, r_unc) : un;
+  }
+  template <class Tile>
+  __device__ __forceinline__ void merge(const Tile& tile) {
+#pragma unroll
+    for (int m = 1; m < Tile::num_threads(); m <<= 1) {
+      const int or1 = tile.shfl_xor(r1, m), oi1 = tile.shfl_xor(i1, m), oun = tile.shfl_xor(un, m);
+      const float oe1 = tile.shfl_xor(e1, m), oe2 = tile.shfl_xor(e2, m);
+      if (or1 < r1) {
+        r1 = or1; i1 = oi1; e1 = oe1; e2 = oe2;
+      } else if (or1 == r1) {
+        e2 = fminf(fminf(e2, oe2), fmaxf(e1, oe1));
+        if (oe1 < e1 || (oe1 == e1 && (unsigned)oi1 < (unsigned)i1)) { e1 = oe1; i1 = oi1; }
+      }
+      un = min(un, oun);
+    }
+  }
+};
+
+struct OrCtx {
+  double s, goal, period, idle;   // exact inputs
+  float sf, goal_f, glo, ghi, oh, P, idle_f, idleP, dE, e_lo, e_hi;
+  int rank_q;
+};
+
+__device__ __forceinline__ void make_or_ctx(OrCtx& o, const DevTable& T, const SpecDev* sp, double s, double idle,
+                                            double goal) {
+  o.s = s; o.goal = goal; o.idle = idle; o.period = xadd(goal, sp->oh);
+  o.sf = (float)s;
+  o.goal_f = (float)goal;
+  o.glo = o.goal_f * (1.0f - 8.0f * kEps);
+  o.ghi = o.goal_f * (1.0f + 8.0f * kEps);
+  o.oh = (float)sp->oh;
+  o.P = (float)o.period;
+  o.idle_f = (float)idle;
+  o.idleP = o.idle_f * o.P;
+  o.dE = 8.0f * kEps * (T.cap_max + o.idle_f) * o.P;
+  o.e_lo = sp->e_f - o.dE;
+  o.e_hi = sp->e_f + o.dE;
+  o.rank_q = sp->rank_q;
+}
+
+// Running per-column state of the FP32 oracle evaluation.
+struct OrRun {
+  bool done;    // some stage of the column completed
+  bool poison;  // a completion test so far was inside the uncertainty band
+  int rank;     // class of the delivered accuracy
+};
+
+// FP32 outcome of one cell (updates the running column state).
+__device__ __forceinline__ void or_cell(const OrCtx& o, const float4& A, const float4& B, OrRun& run, float& E,
+                                        int& rank, bool& met, bool& poison) {
+  const float x = o.sf * B.x;
+  const bool done = x <= o.goal_f;
+  const bool band = x >= o.glo && x <= o.ghi;
+  if (A.w >= 0.0f) {  // traditional cell or first stage of a column
+    run.done = false;
+    run.poison = false;
+    run.rank = cell_rank_qf(B);
+  }
+  run.poison |= band;
+  if (done) {
+    run.done = true;
+    run.rank = cell_rank_a(B);
+  }
+  met = run.done;
+  rank = run.rank;
+  poison = run.poison;
+  const float L = (cell_stage(B) == 0 ? x : fminf(x, o.goal_f)) + o.oh;
+  const float cap = A.y * A.x;  // (cap t) * (1/t)
+  E = fmaf(cap - o.idle_f, fminf(L, o.P), o.idleP);
+}
+
+template <int MAXACC>
+struct OracleScan {
+  Tracker te;       // min-energy level 0 (energy objective)
+  LexTracker lx[3]; // rank-objective levels
+  // refine state
+  int level;
+  float ecut;
+  int rcut;
+  bool all;
+  Key64 best;
+
+  // classification at a level: sure / possible and the lowest possible rank
+  __device__ __forceinline__ void classify(const OrCtx& o, int L, float E, int rank, bool met, bool poison,
+                                           bool& sure, bool& unc, int& r_unc) const {
+    r_unc = poison ? 0 : rank;
+    if (L == 2) { sure = !poison; unc = poison; return; }
+    if (MAXACC) {
+      if (L == 0) {
+        sure = !poison && met && E <= o.e_lo;
+        unc = (poison && E <= o.e_hi) || (!poison && met && E > o.e_lo && E <= o.e_hi);
+      } else {
+        sure = !poison && met;
+        unc = poison;
+      }
+    } else {  // min-energy levels 0/1: met and delivered >= q_goal
+      sure = !poison && met && rank < o.rank_q;
+      unc = poison;
+    }
+  }
+
+  template <int TRACK>
+  __device__ __forceinline__ void scan_cell(const OrCtx& o, int c, float E, int rank, bool met, bool poison) {
+    bool sure, unc;
+    int ru;
+    if (TRACK == TRACK_L2) {
+      classify(o, 2, E, rank, met, poison, sure, unc, ru);
+      lx[2].push(rank, E, sure, unc, ru, c);
+      return;
+    }
+    classify(o, 0, E, rank, met, poison, sure, unc, ru);
+    if (MAXACC) {
+      lx[0].push(rank, E, sure, unc, ru, c);
+      classify(o, 1, E, rank, met, poison, sure, unc, ru);
+      lx[1].push(rank, E, sure, unc, ru, c);
+    } else {
+      te.push(E, sure, unc, c);
+    }
+  }
+
+  __device__ __forceinline__ void refine_cell(const float4* sB, const Cell64* C, const SpecDev* sp, const OrCtx& o,
+                                              int c, float E, int rank, bool met, bool poison) {
+    if (!all) {
+      bool sure, unc;
+      int ru;
+      classify(o, level, E, rank, met, poison, sure, unc, ru);
+      if (!(sure || unc)) return;
+      const bool energy_level = !MAXACC && level != 2;
+      if (energy_level ? !(E <= ecut) : (ru > rcut)) return;
+    }
+    const Outcome x = execute_measure(sB, C, sp, c, o.s, o.goal, o.period, o.idle);
+    // _exact_eval + the level filters of policies.py:171-186
+    if (level != 2 && !x.met) return;
+    if (MAXACC) {
+      if (level == 0 && x.energy > sp->e_goal) return;
+    } else if (level < 2 && x.delivered < sp->q_goal) {
+      return;
+    }
+    const bool acc_obj = level == 2 || MAXACC;
+    Key64 k;
+    k.p0 = acc_obj ? -x.delivered : x.energy;
+    k.p1 = acc_obj ? x.energy : -x.delivered;
+    k.tk = __float_as_uint(sB[c].y);
+    k.cell = c;
+    if (best.cell < 0 || k.less(best)) best = k;
+  }
+};
+
+// Traversal shared by the oracle scan / refine passes (flat at W = 1).
+template <int PASS, int TRACK, int MAXACC, class Tile>
+__device__ __forceinline__ void oracle_pass(const DevTable& T, const float4* __restrict__ sA,
+                                            const float4* __restrict__ sB, const int2* __restrict__ sCol,
+                                            const Cell64* C, const SpecDev* sp, const Tile& tile, const OrCtx& o,
+                                            OracleScan<MAXACC>& S) {
+  const int W = Tile::num_threads();
+  const int lane = tile.thread_rank();
+  auto visit = [&](int c, OrRun& run) {
+    float E;
+    int rank;
+    bool met, poison;
+    or_cell(o, sA[c], sB[c], run, E, rank, met, poison);
+    if (PASS == 0) S.template scan_cell<TRACK>(o, c, E, rank, met, poison);
+    else S.refine_cell(sB, C, sp, o, c, E, rank, met, poison);
+  };
+  if (W == 1) {
+    OrRun run{false, false, 0};
+#pragma unroll 4
+    for (int c = 0; c < T.n_cells; ++c) visit(c, run);
+    return;
+  }
+  for (int c = lane; c < T.n_trad; c += W) {
+    OrRun run{false, false, 0};
+    visit(c, run);
+  }
+  for (int col = lane; col < T.n_any_cols; col += W) {
+    const int2 cd = sCol[col];
+    OrRun run{false, false, 0};
+    for (int k = 0; k < cd.y; ++k) visit(cd.x + k, run);
+  }
+}
+
+template <int MAXACC, class Tile>
+__device__ Decision oracle_decide_t(const DevTable& T, const float4* sA, const float4* sB, const Cell64* C,
+                                    const int2* sCol, const Tile& tile, const SpecDev* sp, const OrCtx& o) {
+  OracleScan<MAXACC> S;
+  S.te.init();
+  S.lx[0].init(); S.lx[1].init(); S.lx[2].init();
+  oracle_pass<0, TRACK_CONSTRAINED>(T, sA, sB, sCol, C, sp, tile, o, S);
+  if (MAXACC) {
+    S.lx[0].merge(tile);
+    S.lx[1].merge(tile);
+  } else {
+    S.te.merge(tile);
+  }
+  const bool empty01 = MAXACC ? (S.lx[0].r1 == 0x7fffffff && S.lx[0].un == 0x7fffffff &&
+                                 S.lx[1].r1 == 0x7fffffff && S.lx[1].un == 0x7fffffff)
+                              : (!(S.te.b1 < kInfF) && !(S.te.un < kInfF));
+  if (empty01) {
+    oracle_pass<0, TRACK_L2>(T, sA, sB, sCol, C, sp, tile, o, S);
+    S.lx[2].merge(tile);
+  }
+  constexpr int NL = MAXACC ? 3 : 2;
+  Decision d{-1, 0, false};
+  int start = -1;
+  bool done = false;
+#pragma unroll
+  for (int li = 0; li < NL; ++li) {
+    const int L = (!MAXACC && li == 1) ? 2 : li;
+    if (done) continue;
+    if (!MAXACC && L == 0) {
+      const Tracker& tr = S.te;
+      const float cut = tr.b1 + 2.0f * o.dE;
+      if (tr.un < kInfF && (!(tr.b1 < kInfF) || tr.un <= cut)) { start = li; done = true; }
+      else if (tr.b1 < kInfF) {
+        if (tr.b2 <= cut) start = li;
+        else { d.cell = tr.i1; d.level = L; }
+        done = true;
+      }
+    } else {
+      const LexTracker& lt = S.lx[L];
+      if (lt.r1 == 0x7fffffff && lt.un == 0x7fffffff) continue;  // empty level
+      if (lt.r1 != 0x7fffffff && lt.un > lt.r1 && lt.e2 > lt.e1 + 2.0f * o.dE) {
+        d.cell = lt.i1;
+        d.level = L;
+      } else {
+        start = li;
+      }
+      done = true;
+    }
+  }
+  if (start < 0) return d;
+#pragma unroll
+  for (int li = 0; li < NL; ++li) {
+    const int L = (!MAXACC && li == 1) ? 2 : li;
+    if (li >= start && d.cell < 0) {
+      S.level = L;
+      const bool e_level = !MAXACC && L == 0;
+      const bool scanned = e_level ? (S.te.b1 < kInfF) : (S.lx[L].r1 != 0x7fffffff);
+      S.all = !scanned && !(e_level ? (S.te.un < kInfF) : (S.lx[L].un != 0x7fffffff));
+      S.ecut = e_level && scanned ? S.te.b1 + 2.0f * o.dE : kInfF;
+      S.rcut = (!e_level && scanned) ? S.lx[L].r1 : 0x7fffffff;
+      S.best.init();
+      oracle_pass<1, TRACK_CONSTRAINED>(T, sA, sB, sCol, C, sp, tile, o, S);
+      S.best.merge(tile);
+      if (S.best.cell >= 0) {
+        d.cell = S.best.cell;
+        d.level = L;
+        d.refined = true;
+      }
+    }
+  }
+  return d;
+}
+
+template <class Tile>
+__device__ __forceinline__ Decision oracle_decide(const DevTable& T, const float4* sA, const float4* sB,
+                                                  const Cell64* C, const int2* sCol, const Tile& tile,
+                                                  const SpecDev* sp, double s, double idle, double goal,
+                                                  bool fp64_all) {
+  if (fp64_all) return oracle_decide_exact(T, sB, C, sCol, tile, sp, s, idle, goal);
+  OrCtx o;
+  make_or_ctx(o, T, sp, s, idle, goal);
+  if (!(o.P > 0.0f) || !isfinite(o.dE)) return oracle_decide_exact(T, sB, C, sCol, tile, sp, s, idle, goal);
+  if (sp->mode == ALERT_MODE_MAX_ACCURACY) return oracle_decide_t<1>(T, sA, sB, C, sCol, tile, sp, o);
+  return oracle_decide_t<0>(T, sA, sB, C, sCol, tile, sp, o);
 }
 
 __device__ __forceinline__ uint32_t pack_decision(int cand, int level, const Outcome& o, bool refined, int phase) {

@@ -271,8 +271,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
     double s;  // true slow-down of this input: consumed only after the decision
     if (PF == PF_ORACLE) {
       s = s_of_raw(tr, s_raw);
-      d = oracle_decide(T, sB, C64, sCol, tile, spec, s, idle, goal);
-      d.refined = false;
+      d = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, idle, goal, fp64_all);
     } else {
       StepCtx x;
       make_ctx(x, spec, C64, f.mu, f.sigma2, f.phi, goal, fp64_all);
@@ -300,7 +299,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
     const AlertOutputs& out = P.out;
     if (writer && out.decision) {
       const long long oidx = stream * out.stream_stride + n * out.step_stride;
-      out.decision[oidx] = pack_decision(__float_as_int(sB[d.cell].z), d.level, o, d.refined, phase);
+      out.decision[oidx] = pack_decision(cell_cand(sB[d.cell]), d.level, o, d.refined, phase);
       if (out.record_dtype == ALERT_DTYPE_F64) {
         if (out.energy) static_cast<double*>(out.energy)[oidx] = o.energy;
         if (out.accuracy) static_cast<double*>(out.accuracy)[oidx] = o.delivered;
@@ -326,7 +325,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
       G.ref += d.refined;
     }
     if (PF == PF_BOTH) {  // OraclePolicy alongside on the same step
-      Decision od = oracle_decide(T, sB, C64, sCol, tile, spec, s, idle, goal);
+      Decision od = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, idle, goal, fp64_all);
       const Outcome oo = execute_measure(sB, C64, spec, od.cell, s, goal, period, idle);
       if (writer && agg) {
         neumaier(G.oe, G.oec, oo.energy);
@@ -336,7 +335,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
       }
       if (writer && out.oracle_decision)
         out.oracle_decision[stream * out.stream_stride + n * out.step_stride] =
-            pack_decision(__float_as_int(sB[od.cell].z), od.level, oo, false, phase);
+            pack_decision(cell_cand(sB[od.cell]), od.level, oo, false, phase);
     }
   }
   if (!writer) return;
@@ -405,19 +404,19 @@ __global__ void __launch_bounds__(256) decide_kernel(const StepParams P, uint32_
   make_ctx(x, spec, T.c64, P.st.mu[i], P.st.sigma2[i], P.st.phi[i], P.goal[i], P.flags & ALERT_FLAG_FP64_ALL);
   Decision d = alert_decide(T, sA, sB, sCol, tile, x, P.kinds, P.flags & ALERT_FLAG_NO_REFINE);
   if (tile.thread_rank() == 0)
-    decision[i] = (uint32_t)__float_as_int(sB[d.cell].z) | ((uint32_t)d.level << 16) | ((uint32_t)d.refined << 26);
+    decision[i] = (uint32_t)cell_cand(sB[d.cell]) | ((uint32_t)d.level << 16) | ((uint32_t)d.refined << 26);
 }
 
 template <int W>
 __global__ void oracle_decide_kernel(const DevTable T, const SpecDev* specs, int n_specs, const int32_t* stream_spec,
                                      const double* s, const double* idle, const double* goal, uint32_t* decision,
-                                     long long n) {
+                                     long long n, bool fp64_all) {
   auto tile = cg::tiled_partition<W>(cg::this_thread_block());
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;
   if (i >= n) return;
   const int si = stream_spec ? stream_spec[i] : (int)(i % n_specs);
-  Decision d = oracle_decide(T, T.cellB, T.c64, T.any_cols, tile, specs + si, s[i], idle[i], goal[i]);
-  if (tile.thread_rank() == 0) decision[i] = (uint32_t)__float_as_int(T.cellB[d.cell].z) | ((uint32_t)d.level << 16);
+  Decision d = oracle_decide(T, T.cellA, T.cellB, T.c64, T.any_cols, tile, specs + si, s[i], idle[i], goal[i], fp64_all);
+  if (tile.thread_rank() == 0) decision[i] = (uint32_t)cell_cand(T.cellB[d.cell]) | ((uint32_t)d.level << 16);
 }
 
 
@@ -429,7 +428,7 @@ cudaError_t launch_decide(const StepParams& P, uint32_t* out, int tpb, size_t sm
 template <int W>
 cudaError_t launch_oracle(const DevTable& T, const SpecDev* specs, int n_specs, const int32_t* stream_spec,
                           const double* s, const double* idle, const double* goal, uint32_t* decision,
-                          long long n, int tpb, cudaStream_t st);
+                          long long n, int tpb, unsigned flags, cudaStream_t st);
 
 template <class K>
 inline cudaError_t set_smem(K kern, size_t smem) {
@@ -466,10 +465,10 @@ inline cudaError_t set_smem(K kern, size_t smem) {
   cudaError_t launch_oracle<W>(const DevTable& T, const SpecDev* specs, int n_specs,                  \
                                const int32_t* stream_spec, const double* s, const double* idle,       \
                                const double* goal, uint32_t* decision, long long n, int tpb,         \
-                               cudaStream_t st) {                                                     \
+                               unsigned flags, cudaStream_t st) {                                     \
     long long blocks = (n * W + tpb - 1) / tpb;                                                       \
     oracle_decide_kernel<W><<<(unsigned)blocks, tpb, 0, st>>>(T, specs, n_specs, stream_spec, s, idle, goal, \
-                                                             decision, n);                           \
+                                                             decision, n, flags & ALERT_FLAG_FP64_ALL);  \
     return cudaGetLastError();                                                                        \
   }
 

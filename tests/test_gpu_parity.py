@@ -338,3 +338,19 @@ def test_phi32_error_bound():
     ref = np.array([0.5 * math.erfc(-v) for v in xs])
     err = np.abs(out.cpu().numpy().astype(np.float64) - ref)
     assert err.max() <= 4.0 * 2.0**-23, err.max()
+
+
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_oracle_fp32_scan_equals_fp64(seed):
+    """The oracle's FP32 scan + FP64 re-rank picks exactly what the all-FP64
+    oracle picks (decisions and every FP64 aggregate), incl. fused alongside."""
+    space, specs, envs = _random_batch(seed, 32, 150, max_dnns=6, max_powers=6)
+    for policy in ("oracle", "alert+oracle"):
+        fast = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64)
+        full = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64,
+                           flags=abi.FLAG_FP64_ALL)
+        np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
+        np.testing.assert_array_equal(fast.agg[:, :abi.AGG_REFINED], full.agg[:, :abi.AGG_REFINED])
+        np.testing.assert_array_equal(fast.agg[:, abi.AGG_OR_ENERGY:], full.agg[:, abi.AGG_OR_ENERGY:])
+        if policy == "alert+oracle":
+            np.testing.assert_array_equal(fast.oracle_decision & 0xFFFF, full.oracle_decision & 0xFFFF)
