@@ -366,12 +366,14 @@ def main():
         peak = pk.value
     clocks = clk.summary()
     peak_nominal = 148 * 128 * 1965e6
-    traffic = None
+    traffic = None  # DRAM bytes per launch, from the committed ncu capture (bytes/decision x decisions)
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(args.config)
-        except ValueError:
+            t = json.loads(tf.read_text()).get(args.config)
+            if t:
+                traffic = t["bytes_per_decision"] * S * N
+        except (ValueError, KeyError):
             traffic = None
     in_bytes = 4 * per_launch + (24 * per_launch if args.records == "f32" else 0)
     roof = {
