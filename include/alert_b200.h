@@ -69,6 +69,8 @@ enum { ALERT_DTYPE_F32 = 0, ALERT_DTYPE_F64 = 1 };
 /* Run flags */
 #define ALERT_FLAG_FP64_ALL 0x1u   /* skip the FP32 scan: every candidate in FP64 (debug / proof) */
 #define ALERT_FLAG_NO_REFINE 0x2u  /* FP32 decision only (measures the refinement cost; not reference-exact) */
+#define ALERT_FLAG_NO_FAST 0x4u    /* disable the min-energy fast scan (full FP32 scan every step; A/B and tests) */
+#define ALERT_FLAG_FAST_ROWS 0x8u  /* fast scan in row mode even for small tables (tests) */
 
 /* Compiled limits */
 #define ALERT_MAX_STAGES 8         /* stages per anytime DNN                   */

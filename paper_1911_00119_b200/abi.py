@@ -15,6 +15,8 @@ POLICY_ALERT, POLICY_ALERT_ANY, POLICY_ALERT_TRAD, POLICY_ORACLE, POLICY_ALERT_W
 DTYPE_F32, DTYPE_F64 = 0, 1
 FLAG_FP64_ALL = 0x1
 FLAG_NO_REFINE = 0x2
+FLAG_NO_FAST = 0x4  # disable the min-energy fast scan (A/B, tests)
+FLAG_FAST_ROWS = 0x8  # fast scan in row mode (default for > 512 traditional cells)
 MAX_STAGES = 8
 MAX_PHASES = 8
 MAX_CANDIDATES = 6144

@@ -34,6 +34,7 @@ struct AlertContext {
   int device = 0;
   int lanes = 0;  // 0 = auto
   int tpb = 64;
+  bool tpb_auto = true;  // alert_set_launch(.., 0): pick the block size from the shared-memory footprint
   int n_sm = 148;
   int max_smem = 227 * 1024;
   std::atomic<long long> launches{0};
@@ -92,6 +93,50 @@ __global__ void observe_kernel(const DevTable T, const AlertFilterConfig cfg, Al
   idle_update(cfg, f, py_min(1.0, xdiv(idle[i], T.power_cap64[power[i]])), ik, -1, nullptr, nullptr);
   st.mu[i] = f.mu; st.sigma2[i] = f.sigma2; st.k_gain[i] = f.k_gain; st.q_noise[i] = f.q_noise;
   st.innov[i] = f.innov; st.phi[i] = f.phi; st.m_var[i] = f.m_var;
+}
+
+// z-thresholds of the min-energy fast scan, one thread per (spec, traditional
+// DNN) (+ one per spec for the pr_threshold bound).  feasible at level 0
+// (selector.py:73-84 with accuracy_blend, predictor.py:68-70) means
+//   fl(fl(Pr a) + fl(fl(1 - Pr) q_fail)) >= q_goal  and  Pr >= pr_th,
+// with Pr = fl(0.5 fl(1 + erf(x / sqrt 2))) (predictor.py:56-65).  In exact
+// arithmetic that implies Phi(z) >= thr - delta, delta covering the FP64
+// roundings of the blend (4 ulp of the largest operand / (a - q_fail)) and of
+// Pr (erf <= 1 ulp, x, the final rounding: 1e-15 absolute), hence
+// z >= Phi^-1(thr - delta) - margin (normcdfinv error).  Results are lower
+// bounds (never excluding a feasible cell); -inf = always possible, 1e10 =
+// never; capped at 7.5 where Pr can round to exactly 1.  Stored in FP32 as
+// z' = z - 20 eps |z| (the margin of fast_prep, alert_device.cuh).
+__device__ inline double zlo_of_prob(double p) {
+  if (!(p > 0.0)) return -kInf;
+  double z = p >= 1.0 ? 7.5 : fmin(normcdfinv(p), 7.5);
+  return z - 1e-9 * (1.0 + fabs(z));
+}
+__global__ void zlo_kernel(const SpecDev* specs, int n_specs, const Cell64* c64, int P, int n_tdnn, float* out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = n_tdnn + 1;
+  if (i >= (long long)n_specs * stride) return;
+  const int s = (int)(i / stride), d = (int)(i % stride);
+  const SpecDev& sp = specs[s];
+  const double zpr = sp.has_pr ? zlo_of_prob(sp.pr_th - 1e-15) : -kInf;
+  double z;
+  if (d == n_tdnn) {
+    z = zpr;
+  } else {
+    const double a = c64[(size_t)d * P].a, qf = c64[(size_t)d * P].qf, q = sp.q_goal;
+    if (!(a > qf)) {
+      z = -kInf;  // accuracy not increasing in Pr: leave it to the certification
+    } else if (q > a * (1.0 + 1e-14) && q > a + 1e-300) {
+      z = kInf;   // acc <= max(a, q_fail) (1 + 4 ulp) < q_goal: never feasible
+    } else {
+      const double m = fmax(1.0, fmax(fabs(a), fmax(fabs(qf), fabs(q))));
+      const double delta = 8.0 * 1.1102230246251565e-16 * m / (a - qf) + 1e-15;
+      z = zlo_of_prob((q - qf) / (a - qf) - delta);
+    }
+    z = fmax(z, zpr);
+  }
+  const float zf = z == kInf ? 1e10f : (float)z;
+  out[i] = fmaf(-20.0f * kEps, fabsf(zf), zf);
 }
 
 __global__ void state_init_kernel(AlertState st, AlertFilterConfig cfg, double phi0, long long n) {
@@ -186,6 +231,7 @@ int alert_set_launch(AlertContext* ctx, int lanes, int tpb) {
     return fail(ALERT_ERR_INVALID_ARGUMENT, "threads_per_block must be a multiple of 32 in [32, 256]");
   ctx->lanes = lanes;
   ctx->tpb = tpb ? tpb : 64;
+  ctx->tpb_auto = tpb == 0;
   return ALERT_OK;
 }
 
@@ -424,8 +470,26 @@ static size_t table_smem(const AlertTable* tb, int W) {
 
 // Staging decisions of run_kernel: specs, FP64 cells and the per-segment
 // idle-ratio table go to shared memory when small (see SmemLayout).
-static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_specs, int tpb, int W, RunParams& P) {
+static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_specs, int tpb, int W, RunParams& P,
+                        int policy = ALERT_POLICY_ALERT, unsigned flags = 0) {
   const DevTable& T = tb->dev;
+  // min-energy fast scan (fast_min_energy): needs some min-energy spec, row /
+  // column indices that fit the 6-bit key field, and the ALERT policy family
+  bool any_min_energy = false, all_min_energy = true;
+  for (int k = 0; k < n_specs; ++k) {
+    any_min_energy |= specs[k].mode == ALERT_MODE_MIN_ENERGY;
+    all_min_energy &= specs[k].mode == ALERT_MODE_MIN_ENERGY;
+  }
+  P.min_energy_only = all_min_energy;
+  const int n_tdnn = T.n_powers > 0 ? T.n_trad / T.n_powers : 0;
+  P.zlo = nullptr;
+  P.fast_smem = 0;
+  // row mode for large tables (no staged per-cell rows / per-tile thresholds)
+  P.fast_rows = T.n_trad > 512 || (flags & ALERT_FLAG_FAST_ROWS);
+  if (any_min_energy && policy != ALERT_POLICY_ORACLE && !(flags & (ALERT_FLAG_NO_FAST | ALERT_FLAG_FP64_ALL)) &&
+      ALERT_MAX_STAGES <= 8 &&
+      (P.fast_rows || (size_t)(tpb / W) * (size_t)(n_tdnn + 1) * 2 * sizeof(float) <= 16 * 1024))
+    P.fast_smem = 1;  // alert_run computes the thresholds (zlo_kernel) and sets P.zlo
   P.c64_smem = T.n_cells <= kC64SmemMax;
   P.ratio_smem = T.n_powers <= kRatioSmemMax &&
                  (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;
@@ -440,7 +504,9 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
 static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const RunParams& P) {
   const DevTable& T = tb->dev;
   SmemLayout L(T.n_cells, T.n_any_cols, tpb / W, P.c64_smem ? T.n_cells : 0, tpb / W,
-               P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W);
+               P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
+               (P.fast_smem && !P.fast_rows) ? T.n_trad / T.n_powers : 0,
+               (P.fast_smem && !P.fast_rows) ? T.n_trad : 0);
   return L.total;
 }
 
@@ -561,6 +627,8 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
     return fail(ALERT_ERR_INVALID_TRACE, "alert_run: step range outside the trace buffer");
   if (stream_begin < 0 || stream_end < stream_begin)
     return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: bad stream range");
+  if (stream_end > 0x7fffffffLL || step_end > 0x7fffffffLL)
+    return fail(ALERT_ERR_UNSUPPORTED, "alert_run: stream / step indices must fit in 31 bits");
   if (!tr->stream_row && stream_end > tr->n_rows)
     return fail(ALERT_ERR_INVALID_TRACE, "alert_run: more streams than trace rows and no stream_row map");
   if (!st.mu || !st.sigma2 || !st.k_gain || !st.q_noise || !st.innov || !st.phi || !st.m_var || !st.group_budget ||
@@ -573,8 +641,25 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   if (stream_end == stream_begin || step_end == step_begin) return ALERT_OK;
   int W = pick_lanes(ctx, tb);
   RunParams P;
-  run_staging(tb, specs, n_specs, ctx->tpb, W, P);
-  size_t smem = run_smem(tb, n_specs, ctx->tpb, W, P);
+  auto stage = [&](int tpb) {
+    run_staging(tb, specs, n_specs, tpb, W, P, policy, flags);
+    size_t sm = run_smem(tb, n_specs, tpb, W, P);
+    if ((int)sm > ctx->max_smem && P.fast_smem) {  // no room for the fast-scan tables
+      P.fast_smem = 0;
+      sm = run_smem(tb, n_specs, tpb, W, P);
+    }
+    return sm;
+  };
+  // Block size: 64 threads by default (fine-grained waves for ~10^4-10^5
+  // streams); a large table (shared memory per block > 40 KB) with enough
+  // streams gets 256-thread blocks so the staged table is shared by 4x more
+  // tiles and occupancy is not capped by shared memory.
+  int tpb = ctx->tpb;
+  size_t smem = stage(tpb);
+  if (ctx->tpb_auto && smem > 40 * 1024 && (stream_end - stream_begin) * W >= 148LL * 2 * 256) {
+    tpb = 256;
+    smem = stage(tpb);
+  }
   if ((int)smem > ctx->max_smem) return fail(ALERT_ERR_UNSUPPORTED, "alert_run: table exceeds shared memory");
   idle_table(*cfg, P);
   CUDA_TRY(cudaSetDevice(ctx->device));
@@ -598,8 +683,20 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   P.step_begin = step_begin;
   P.step_end = step_end;
   int pf = policy == ALERT_POLICY_ORACLE ? PF_ORACLE : policy == ALERT_POLICY_ALERT_WITH_ORACLE ? PF_BOTH : PF_ALERT;
-  r = dispatch_run(W, pf, P, ctx->tpb, smem, s);
+  float* dzlo = nullptr;
+  if (P.fast_smem) {  // fast scan staged by run_staging: compute the thresholds on the stream
+    const int n_tdnn = tb->dev.n_trad / tb->dev.n_powers;
+    const long long nz = (long long)n_specs * (n_tdnn + 1);
+    CUDA_TRY(cudaMallocAsync((void**)&dzlo, sizeof(float) * nz, s));
+    zlo_kernel<<<(unsigned)((nz + 127) / 128), 128, 0, s>>>(dspecs, n_specs, tb->dev.c64, tb->dev.n_powers, n_tdnn,
+                                                          dzlo);
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches++;
+    P.zlo = dzlo;
+  }
+  r = dispatch_run(W, pf, P, tpb, smem, s);
   cudaFreeAsync(dspecs, s);
+  if (dzlo) cudaFreeAsync(dzlo, s);
   if (r) return r;
   ctx->launches++;
   return ALERT_OK;

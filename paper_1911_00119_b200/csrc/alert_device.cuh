@@ -148,7 +148,7 @@ struct StepCtx {
   const Cell64* c64;  // FP64 cell data (shared memory when it fits)
   // FP32 scan inputs: x = (goal/t - mu) * inv_sig_s  (= z / sqrt 2),
   //                   E = (cap t) * max(mu_e, phig / t + ompmu)
-  float goal_f, mu_f, inv_sig_s, mu_e, ompmu, phig;
+  float goal_f, mu_f, inv_sig_s, mu_e, ompmu, phig, sig_f;
   // FP32 error bounds
   float d_pr, d_acc, d_erel;
   // thresholds with margins
@@ -156,6 +156,15 @@ struct StepCtx {
   bool fp64_all;
   unsigned sv;   // shared-space address of the tile's per-cell FP32 objectives
   bool has_sv;   // stored objectives enabled
+  // min-energy fast scan (fast_min_energy): per-step feasibility thresholds
+  // of the traditional DNNs, tile-shared, element d at tT[d * tS]
+  bool fast;
+  const float* tT;
+  int tS;
+  const float4* sF;  // traditional cells {1/t, cap t, byte offset of the DNN's threshold in tT, 0}
+  const float* zrow; // row mode (large tables): the spec's z' per traditional DNN (global, L1)
+  float hs, hm;      // T_d = fma(z'_d, hs, hm)
+  float Tpr;     // same for the pr_threshold z-bound (anytime cells)
 };
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -172,6 +181,13 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
   x.c64 = c64;
   x.sv = 0;
   x.has_sv = false;
+  x.fast = false;
+  x.tT = nullptr;
+  x.tS = 0;
+  x.sF = nullptr;
+  x.zrow = nullptr;
+  x.hs = x.hm = 0.f;
+  x.Tpr = -kInfF;
   x.mu = mu;
   x.sig = sigma2;  // holds sigma2 until ensure_fp64()
   x.phi = phi;
@@ -183,6 +199,7 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
   const float inv_sig = rsqrt_approx(s2f);  // MUFU.RSQ, rel. error <= 2 ulp
   x.inv_sig_s = inv_sig * 0.70710678118654752f;
   const float sig_f = s2f * inv_sig;
+  x.sig_f = sig_f;
   x.mu_e = sp->has_pr ? fmaf(sp->zq_f, sig_f, x.mu_f) : x.mu_f;  // predictor.py:140
   const float phi_f = (float)phi;
   x.ompmu = (1.0f - phi_f) * x.mu_e;
@@ -493,6 +510,229 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
   }
 }
 
+// --------------------------------------------------------------------------
+// Min-energy fast scan (level 0 of selector.py:102-131 in MINIMIZE_ENERGY).
+//
+// The level-0 objective is the energy, which needs no Phi.  Feasibility of a
+// traditional cell, acc = Pr a + (1 - Pr) q_fail >= q_goal (and Pr >= pr_th),
+// is a z-threshold per (spec, DNN): z >= Zlo_d (zlo_kernel, FP64, widened by
+// the reference's rounding).  Per step, Zlo_d becomes an additive threshold
+// T_d = H (mu + Zlo_d sigma - slack) so that, per cell, ONE sign-exact FFMA
+//   pen = T_d - H goal / t
+// is <= 0 for every cell the reference can find feasible; pen is folded into
+// the energy's max (FMNMX3), so an excluded cell just gets a huge key.
+// Anytime stages keep the running Phi-based expected accuracy (predict32) and
+// are penalised from it the same way.  Keys are the energy with the cell's
+// index within its row / column in the 6 low mantissa bits; a running top-2
+// of keys (P1, P2) plus the row id of P1 is all the per-cell state.
+//
+// The decision is CERTIFIED only if P1's cell is surely feasible (FP32 check
+// with the same margins as the full scan) and P2 exceeds P1 by more than the
+// FP32 energy error and the key truncation: then every other feasible cell
+// has a strictly larger FP64 energy and P1 is the reference's choice.
+// Otherwise (near-ties, boundary cells, empty level 0) the full scan runs.
+constexpr float kPenH = 1099511627776.0f;  // 2^40: sign-exact scaling of the penalty
+#ifndef ALERT_FAST_CHUNK
+#define ALERT_FAST_CHUNK 8  // traditional cells in flight per lane (power of two <= 8)
+#endif
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// key = energy bits with the low 3 mantissa bits replaced by idx < 8: one
+// LOP3 (select by the immediate mask; idx in a register)
+__device__ __forceinline__ float pack_key(float e, unsigned idx) {
+  unsigned r;
+  asm("lop3.b32 %0, %1, 0xfffffff8, %2, 0xE2;" : "=r"(r) : "r"(__float_as_uint(e)), "r"(idx));
+  return __uint_as_float(r);
+}
+
+struct Top2 {
+  float p1, p2;
+  int blk;
+  __device__ __forceinline__ void push(float k) {
+    p2 = fminf(p2, fmaxf(p1, k));
+    p1 = fminf(p1, k);
+  }
+  __device__ __forceinline__ void push2(float a, float b) {
+    const float lo = fminf(a, b), hi = fmaxf(a, b);
+    p2 = fmin3(fmaxf(p1, lo), p2, hi);
+    p1 = fminf(p1, lo);
+  }
+  template <class Tile>
+  __device__ __forceinline__ void merge(const Tile& tile) {
+#pragma unroll
+    for (int m = 1; m < Tile::num_threads(); m <<= 1) {
+      const float o1 = tile.shfl_xor(p1, m), o2 = tile.shfl_xor(p2, m);
+      const int ob = tile.shfl_xor(blk, m);
+      p2 = fmin3(p2, o2, fmaxf(p1, o1));
+      if (o1 < p1 || (o1 == p1 && ob < blk)) blk = ob;
+      p1 = fminf(p1, o1);
+    }
+  }
+};
+
+// Per-step thresholds T_d = H (z'_d sigma + mu') (and the pr_threshold
+// bound for anytime cells): one FFMA per DNN.  z' = z - 20 eps |z| (zlo_kernel)
+// and mu' = mu - 20 eps |mu| absorb the FP32 rounding of mu, sigma (rsqrt),
+// goal, 1/t, the threshold FFMA and of z itself: for every cell
+// the reference can find feasible, H goal / t >= T_d holds in FP32.
+template <class Tile>
+__device__ __forceinline__ void fast_prep(StepCtx& x, const Tile& tile, const float* zt, float* tT, int tS,
+                                          int n_tdnn, float zpr, const float* zrow) {
+  x.hs = x.sig_f * kPenH;
+  x.hm = fmaf(-20.0f * kEps, fabsf(x.mu_f), x.mu_f) * kPenH;
+  x.Tpr = fmaf(zpr, x.hs, x.hm);
+  if (zrow) {  // row mode: thresholds computed per DNN inside the scan
+    x.zrow = zrow;
+    return;
+  }
+  for (int d = tile.thread_rank(); d < n_tdnn; d += Tile::num_threads()) tT[d * tS] = fmaf(zt[d * tS], x.hs, x.hm);
+  x.tT = tT;
+  x.tS = tS;
+  if (Tile::num_threads() > 1) tile.sync();
+}
+
+// FP32 sureness of one cell at min-energy level 0 (the full scan's margins).
+__device__ __forceinline__ bool fast_sure(const DevTable& T, const float4* sA, const float4* sB, const StepCtx& x,
+                                          int c, bool has_pr) {
+  const int stage = cell_stage(sB[c]);
+  const int first = stage == 0 ? c : c - (stage - 1);
+  float acc = sA[first].w, pr = 0.f;
+  for (int k = first; k <= c; ++k) {
+    const float4 A = sA[k];
+    pr = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
+    acc = fmaf(pr, A.z, acc);
+  }
+  return acc >= x.q_hi && (!has_pr || pr >= x.th_hi);
+}
+
+template <bool HAS_PR, class Tile>
+__device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4* __restrict__ sA,
+                                                const float4* __restrict__ sB, const int2* __restrict__ sCol,
+                                                const Tile& tile, const StepCtx& x, int kinds, Decision& d) {
+  const int W = Tile::num_threads();
+  const int lane = tile.thread_rank();
+  const float mgH = -x.goal_f * kPenH;
+  Top2 t{kInfF, kInfF, -1};
+  // Traditional cells: flat loop, 8 cells in flight per lane; the key index
+  // is the position u = (c / W) & 7 of the cell in its lane's chunk (staged in
+  // sF[c].w), the chunk's first cell is recorded when P1 improves.  Each
+  // cell's DNN threshold is read through the byte offset staged in sF[c].z.  Anytime columns: key index = stage,
+  // recorded cell = the column's first stage.
+  if ((kinds & 1) && x.zrow) {
+    // row mode (large tables): DNN-major, lanes split the powers of a row in
+    // chunks of 8 (masked at the row end); T_d from the spec's z' (L1), the
+    // next DNN's z' in flight while the current row is scanned
+    const int P = T.n_powers;
+    const int n_tdnn = T.n_trad / P;
+    float zn = __ldg(x.zrow);
+    for (int dn = 0; dn < n_tdnn; ++dn) {
+      const float Td = fmaf(zn, x.hs, x.hm);
+      if (dn + 1 < n_tdnn) zn = __ldg(x.zrow + dn + 1);
+      const float4* row = sA + dn * P;  // padded table: reads past the row are masked
+      for (int p0 = lane; p0 < P; p0 += 8 * W) {
+        const float s1 = t.p1;
+        float k[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float4 A = row[p0 + u * W];
+          const float kk = pack_key(A.y * fmax3(x.mu_e, fmaf(x.phig, A.x, x.ompmu), fmaf(mgH, A.x, Td)), u);
+          k[u] = p0 + u * W < P ? kk : kInfF;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) t.push2(k[u], k[u + 1]);
+        if (t.p1 != s1) t.blk = dn * P + p0;
+      }
+    }
+  } else if (kinds & 1) {
+    const char* tb = reinterpret_cast<const char*>(x.tT);
+    const float4* sF = x.sF;
+    auto key_of = [&](const float4& F) {  // F.w = the cell's position in its chunk
+      const float Td = *reinterpret_cast<const float*>(tb + __float_as_int(F.z));
+      return pack_key(F.y * fmax3(x.mu_e, fmaf(x.phig, F.x, x.ompmu), fmaf(mgH, F.x, Td)), __float_as_uint(F.w));
+    };
+    const int n = T.n_trad;
+    constexpr int K = ALERT_FAST_CHUNK;
+    int c = lane;
+    for (; c + (K - 1) * W < n; c += K * W) {
+      const float s1 = t.p1;
+      float k[K];
+#pragma unroll
+      for (int u = 0; u < K; ++u) k[u] = key_of(sF[c + u * W]);
+#pragma unroll
+      for (int u = 0; u < K; u += 2) t.push2(k[u], k[u + 1]);
+      if (t.p1 != s1) t.blk = c;
+    }
+    if (c < n) {  // < K cells left: the padded table is read past the end, keys masked
+      const float s1 = t.p1;
+      float k[K];
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        const float kk = key_of(sF[c + u * W]);
+        k[u] = c + u * W < n ? kk : kInfF;
+      }
+#pragma unroll
+      for (int u = 0; u < K; u += 2) t.push2(k[u], k[u + 1]);
+      if (t.p1 != s1) t.blk = c;
+    }
+  }
+  if (kinds & 2) {
+    const float qloH = x.q_lo * kPenH;
+    auto any_key = [&](const float4& A, float& acc, unsigned idx) {
+      const float pr = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
+      acc = fmaf(pr, A.z, acc);
+      float pen = fmaf(-kPenH, acc, qloH);
+      if (HAS_PR) pen = fmaxf(pen, fmaf(mgH, A.x, x.Tpr));
+      return pack_key(A.y * fmax3(x.mu_e, fmaf(x.phig, A.x, x.ompmu), pen), idx);
+    };
+    if (W == 1) {  // one flat loop over every anytime cell, 4 in flight; A.w >= 0 starts a column
+      float carry = 0.f;
+      for (int c = T.n_trad; c < T.n_cells; c += 4) {
+        const float s1 = t.p1;
+        float k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 A = sA[c + u];  // padded table
+          float acc = A.w >= 0.0f ? A.w : carry;
+          const float kk = any_key(A, acc, u);
+          carry = acc;
+          k[u] = c + u < T.n_cells ? kk : kInfF;
+        }
+        t.push2(k[0], k[1]);
+        t.push2(k[2], k[3]);
+        if (t.p1 != s1) t.blk = c;
+      }
+    } else {
+      for (int col = lane; col < T.n_any_cols; col += W) {
+        const int2 cd = sCol[col];
+        const float s1 = t.p1;
+        float acc = sA[cd.x].w;
+        for (int k = 0; k < cd.y; ++k) t.push(any_key(sA[cd.x + k], acc, (unsigned)k));
+        if (t.p1 != s1) t.blk = cd.x;
+      }
+    }
+  }
+  t.merge(tile);
+  if (!(t.p1 < kInfF) || t.blk < 0) return false;
+  const float cut = t.p1 + t.p1 * (4.0f * x.d_erel + 3.1e-5f);  // 2^-15 >> truncation of both keys
+  if (!(t.p2 > cut)) return false;
+  const int idx = (int)(__float_as_uint(t.p1) & 7u);
+  const int c = t.blk < T.n_trad ? t.blk + idx * W : t.blk + idx;
+  if (!fast_sure(T, sA, sB, x, c, HAS_PR)) return false;
+  d.cell = c;
+  d.level = 0;
+  d.refined = false;
+  return true;
+}
+
 // Re-rank pass from the stored FP32 objectives (no re-scan): the same
 // cell-to-lane assignment as cell_pass, so each lane reads what it wrote.
 template <int MODE, bool HAS_PR, class Tile>
@@ -523,11 +763,12 @@ __device__ __forceinline__ void refine_stored(const DevTable& T, const float4* _
     }
 }
 
-// AlertPolicy.decide (policies.py:97-103) for the tile's stream.
+// AlertPolicy.decide (policies.py:97-103) for the tile's stream: the full
+// FP32 scan + FP64 re-rank.
 template <int MODE, bool HAS_PR, class Tile>
-__device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const float4* sB,
-                                   const int2* sCol, const Tile& tile, StepCtx& x, int kinds,
-                                   bool no_refine) {
+__device__ __forceinline__ Decision alert_decide_full(const DevTable& T, const float4* sA, const float4* sB,
+                                                      const int2* sCol, const Tile& tile, StepCtx& x, int kinds,
+                                                      bool no_refine) {
   AlertScan<MODE, HAS_PR> S;
 #pragma unroll
   for (int l = 0; l < 3; ++l) S.t[l].init();
@@ -603,16 +844,48 @@ __device__ Decision alert_decide_t(const DevTable& T, const float4* sA, const fl
   return d;
 }
 
-template <class Tile>
+// Mode sets compiled into a kernel: every mode, or min-energy only (smaller
+// code and register footprint when every spec of a launch minimises energy).
+enum { MS_ALL = 0, MS_MIN_ENERGY = 1 };
+
+// The full scan as an out-of-line call: in the min-energy kernel it runs only
+// when the fast scan cannot certify (rare), so its registers are saved around
+// the call instead of being reserved (or spilled) across the whole step loop.
+template <int MODE, bool HAS_PR, class Tile>
+__device__ __noinline__ Decision alert_decide_full_call(const DevTable& T, const float4* sA, const float4* sB,
+                                                        const int2* sCol, Tile tile, StepCtx x, int kinds,
+                                                        bool no_refine) {
+  return alert_decide_full<MODE, HAS_PR>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+}
+
+template <int MODE, bool HAS_PR, bool OUTLINE, class Tile>
+__device__ __forceinline__ Decision alert_decide_t(const DevTable& T, const float4* sA, const float4* sB,
+                                                   const int2* sCol, const Tile& tile, StepCtx& x, int kinds,
+                                                   bool no_refine) {
+  if (MODE == ALERT_MODE_MIN_ENERGY && x.fast && !x.fp64_all) {
+    Decision d{-1, 0, false};
+    if (fast_min_energy<HAS_PR>(T, sA, sB, sCol, tile, x, kinds, d)) return d;
+  }
+  if (OUTLINE) return alert_decide_full_call<MODE, HAS_PR>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+  return alert_decide_full<MODE, HAS_PR>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+}
+
+template <int MS = MS_ALL, class Tile>
 __device__ __forceinline__ Decision alert_decide(const DevTable& T, const float4* sA, const float4* sB,
                                                  const int2* sCol, const Tile& tile, StepCtx& x,
                                                  int kinds, bool no_refine) {
-  if (x.spec->mode == ALERT_MODE_MIN_ENERGY) {
-    if (x.spec->has_pr) return alert_decide_t<ALERT_MODE_MIN_ENERGY, true>(T, sA, sB, sCol, tile, x, kinds, no_refine);
-    return alert_decide_t<ALERT_MODE_MIN_ENERGY, false>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+#ifndef ALERT_OUTLINE_FULL
+#define ALERT_OUTLINE_FULL 0
+#endif
+  constexpr bool OUT = ALERT_OUTLINE_FULL && MS == MS_MIN_ENERGY;
+  if (MS == MS_MIN_ENERGY || x.spec->mode == ALERT_MODE_MIN_ENERGY) {
+    if (x.spec->has_pr)
+      return alert_decide_t<ALERT_MODE_MIN_ENERGY, true, OUT>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+    return alert_decide_t<ALERT_MODE_MIN_ENERGY, false, OUT>(T, sA, sB, sCol, tile, x, kinds, no_refine);
   }
-  if (x.spec->has_pr) return alert_decide_t<ALERT_MODE_MAX_ACCURACY, true>(T, sA, sB, sCol, tile, x, kinds, no_refine);
-  return alert_decide_t<ALERT_MODE_MAX_ACCURACY, false>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+  if (x.spec->has_pr)
+    return alert_decide_t<ALERT_MODE_MAX_ACCURACY, true, false>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+  return alert_decide_t<ALERT_MODE_MAX_ACCURACY, false, false>(T, sA, sB, sCol, tile, x, kinds, no_refine);
 }
 
 // --------------------------------------------------------------------------

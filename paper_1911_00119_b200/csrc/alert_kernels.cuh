@@ -26,6 +26,12 @@ struct RunParams {
   unsigned flags;
   int kinds;
   int c64_smem, ratio_smem, sv_smem;  // staging decisions (host computed)
+  int min_energy_only;                 // every spec minimises energy: MS_MIN_ENERGY kernel
+  // min-energy fast scan: per (spec, traditional DNN) z-thresholds, row
+  // stride n_tdnn + 1 (last = pr_threshold bound), from zlo_kernel; null = off
+  const float* zlo;
+  int fast_smem;  // host: shared-memory slots for the fast scan staged
+  int fast_rows;  // fast scan in row mode (large tables): no staged rows / thresholds
   long long stream_begin, stream_end, step_begin, step_end;
   // Idle-filter gains (estimator.py:123-125) do not depend on the data: the
   // sequence M_k (state after k updates from m0) and W_k reaches an exact FP64
@@ -36,15 +42,23 @@ struct RunParams {
   double idle_m[kIdleTab];
 };
 
+// Per-thread cold state of run_kernel (shared memory): touched at segment
+// changes, by group specs, and once per step for the idle power.
+struct ColdState {
+  double budget, idle;
+  long long seg0;
+  int count, seg, nseg, phase;
+};
+
 // Shared-memory layout of run_kernel (host and device compute it identically).
 struct SmemLayout {
-  size_t B, col, spec, c64, ratio, agg, sv, slot, total;
+  size_t B, col, spec, c64, ratio, agg, sv, fz, ff, cold, slot, total;
   __host__ __device__ static size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
   // pad = look-ahead rows past the end of the cell / column tables for a tile
   // width W: 2 chunks of 4 cells (see cell_pass), so 8 W + 8.
   __host__ __device__ static int pad_rows(int W) { return 8 * W + 8; }
   __host__ __device__ SmemLayout(int n_cells, int n_cols, int n_spec, int n_c64, int n_tiles, int n_ratio,
-                                 size_t agg_bytes, int n_sv, int W) {
+                                 size_t agg_bytes, int n_sv, int W, int n_fz = 0, int n_ff = 0) {
     B = sizeof(float4) * (size_t)(n_cells + pad_rows(W));
     col = B + sizeof(float4) * (size_t)n_cells;
     spec = up16(col + sizeof(int2) * (size_t)(n_cols + pad_rows(W)));
@@ -52,7 +66,10 @@ struct SmemLayout {
     ratio = up16(c64 + sizeof(Cell64) * (size_t)n_c64);
     agg = up16(ratio + sizeof(double) * (size_t)n_tiles * (size_t)n_ratio);
     sv = up16(agg + agg_bytes * (size_t)n_tiles);
-    slot = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);
+    fz = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);  // 2 x [n_fz][n_tiles]: Z, T
+    ff = up16(fz + 2 * sizeof(float) * (size_t)n_tiles * (size_t)n_fz);  // fast-scan traditional cells
+    cold = up16(ff + (n_ff ? sizeof(float4) * (size_t)(n_ff + pad_rows(W)) : 0));
+    slot = up16(cold + sizeof(ColdState) * (size_t)n_tiles * (size_t)W);
     total = up16(slot + 16 * (size_t)n_tiles * (size_t)W);  // two 8-byte trace slots per thread
   }
 };
@@ -101,6 +118,7 @@ struct TileAgg {
 
 enum { PF_ALERT = 0, PF_ORACLE = 1, PF_BOTH = 2 };  // policy families
 
+
 // Close the current segment: per-phase slot (phase ids < ALERT_MAX_PHASES) and
 // overall violation counts.
 __device__ __forceinline__ void flush_segment(TileAgg& g, double* agg, int phase) {
@@ -135,13 +153,23 @@ __device__ __forceinline__ void fill_ratios(const DevTable& T, const Tile& tile,
 
 // The fused closed loop (simulator.run, simulator.py:461-507): one tile of W
 // lanes per stream, filter state in registers for the whole step range.
-template <int W, int PF>
-__global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
+// Register budget: 128 (16 warps / SM) for the general kernels; the
+// min-energy-only kernel gets ALERT_MINE_REGS (default 144: 14 warps / SM,
+// still one wave for 65,536 one-lane streams in 64-thread blocks) so its
+// per-step state stays out of local memory.
+#ifndef ALERT_MINE_REGS
+#define ALERT_MINE_REGS 128
+#endif
+template <int W, int PF, int MS>
+__global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_MINE_REGS : 128)
+    run_kernel(const RunParams P) {
   extern __shared__ float4 smem[];
   const DevTable& T = P.T;
   const int n_tiles = blockDim.x / W;
+  const int n_tdnn = T.n_trad / T.n_powers;
   const SmemLayout L(T.n_cells, T.n_any_cols, n_tiles, P.c64_smem ? T.n_cells : 0, n_tiles,
-                     P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W);
+                     P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
+                     (P.zlo && !P.fast_rows) ? n_tdnn : 0, (P.zlo && !P.fast_rows) ? T.n_trad : 0);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
   float4* sB = reinterpret_cast<float4*>(base + L.B);
@@ -151,24 +179,38 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   double* sRatio = reinterpret_cast<double*>(base + L.ratio);
   TileAgg* sAgg = reinterpret_cast<TileAgg*>(base + L.agg);
   float* sV = reinterpret_cast<float*>(base + L.sv);
+  ColdState* sCold = reinterpret_cast<ColdState*>(base + L.cold);
   load_table_smem(T, sA, sB, sCol);
   if (P.c64_smem)
     for (int i = threadIdx.x; i < T.n_cells; i += blockDim.x) sC64[i] = T.c64[i];
+  float4* sF = reinterpret_cast<float4*>(base + L.ff);
+  if (P.zlo && !P.fast_rows)  // fast-scan rows {1/t, cap t, byte offset of the DNN threshold, (c / W) & 7}, padded
+    for (int i = threadIdx.x; i < T.n_trad + SmemLayout::pad_rows(W); i += blockDim.x) {
+      const bool in = i < T.n_trad;
+      const int off = in ? (i / T.n_powers) * n_tiles * (int)sizeof(float) : 0;
+      sF[i] = make_float4(in ? T.cellA[i].x : 0.f, in ? T.cellA[i].y : 0.f, __int_as_float(off),
+                          __int_as_float((i / W) & (ALERT_FAST_CHUNK - 1)));
+    }
   __syncthreads();
   const Cell64* C64 = P.c64_smem ? sC64 : T.c64;
 
   auto tile = cg::tiled_partition<W>(cg::this_thread_block());
-  const long long stream = P.stream_begin + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;
-  if (stream >= P.stream_end) return;
+  const long long stream_ll = P.stream_begin + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;
+  if (stream_ll >= P.stream_end) return;
+  const int stream = (int)stream_ll;  // < 2^31 (checked on the host)
   const bool writer = tile.thread_rank() == 0;
-  TileAgg& G = sAgg[threadIdx.x / W];
-  double* ratio_tab = P.ratio_smem ? sRatio + (size_t)(threadIdx.x / W) * T.n_powers : nullptr;
-  const unsigned sv_tile = (unsigned)__cvta_generic_to_shared(sV + (size_t)(threadIdx.x / W) * T.n_cells);
+  const int tid = threadIdx.x / W;  // tile index in the block
+  TileAgg& G = sAgg[tid];
+  // Cold per-stream state (group budget, segment cursor, idle power) lives in
+  // the thread's shared slots, not in registers across the step loop: the
+  // step loop's register budget goes to the scan.
+  ColdState& cs = sCold[threadIdx.x];
+  const unsigned sv_tile = (unsigned)__cvta_generic_to_shared(sV + (size_t)tid * T.n_cells);
 
-  const int si = P.stream_spec ? P.stream_spec[stream] : (int)(stream % P.n_specs);
+  const int si = P.stream_spec ? P.stream_spec[stream] : (int)(stream_ll % P.n_specs);
   // the stream's spec, copied once into the tile's shared slot (all per-step
   // spec reads are then shared-memory loads)
-  SpecDev* spec = sSpec + threadIdx.x / W;
+  SpecDev* spec = sSpec + tid;
   {
     const float4* src = reinterpret_cast<const float4*>(P.specs + si);
     float4* dst = reinterpret_cast<float4*>(spec);
@@ -176,7 +218,20 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
     tile.sync();
   }
   const AlertTrace& tr = P.tr;
-  const long long row = tr.stream_row ? tr.stream_row[stream] : stream;
+  const long long row = tr.stream_row ? tr.stream_row[stream] : stream_ll;
+  // min-energy fast scan: the stream's z-thresholds, copied once into the
+  // tile's interleaved shared slots (element d at [d * n_tiles + tile])
+  const bool fast = P.zlo && spec->mode == ALERT_MODE_MIN_ENERGY;
+  float zpr = -kInfF;
+  if (fast) {
+    const float* zrow = P.zlo + (size_t)si * (n_tdnn + 1);
+    zpr = zrow[n_tdnn];
+    if (!P.fast_rows) {
+      float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
+      for (int d = tile.thread_rank(); d < n_tdnn; d += W) fzZ[d * n_tiles] = zrow[d];
+      if (W > 1) tile.sync();
+    }
+  }
 
   Filter f;
   f.mu = P.st.mu[stream];
@@ -191,22 +246,27 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   if (P.idle_fix >= 0)
     for (int k = 0; k <= P.idle_fix; ++k)
       if (P.idle_m[k] == f.m_var) { ik = k; break; }
-  double budget = P.st.group_budget[stream];
-  int count = P.st.group_count[stream];
-  const int group_size = spec->group_size;
+  cs.budget = P.st.group_budget[stream];
+  cs.count = P.st.group_count[stream];
 
-  // segment (phase) tracking
-  const int nseg = tr.n_segments[row];
-  const long long seg0 = row * tr.max_segments;  // segment arrays are re-read only at segment changes
-  int seg = 0;
-  while (seg + 1 < nseg && P.step_begin >= tr.seg_end[seg0 + seg]) ++seg;
-  int cur_end = tr.seg_end[seg0 + seg];
-  int phase = tr.seg_phase[seg0 + seg];
-  double idle = tr.seg_idle[seg0 + seg];
-  if (ratio_tab) fill_ratios(T, tile, ratio_tab, idle);
+  // segment (phase) tracking; only cur_end stays in a register
+  {
+    const int nseg = tr.n_segments[row];
+    const long long seg0 = row * tr.max_segments;
+    int seg = 0;
+    while (seg + 1 < nseg && P.step_begin >= tr.seg_end[seg0 + seg]) ++seg;
+    cs.seg0 = seg0;
+    cs.nseg = nseg;
+    cs.seg = seg;
+    cs.phase = tr.seg_phase[seg0 + seg];
+    cs.idle = tr.seg_idle[seg0 + seg];
+  }
+  int cur_end = cs.seg + 1 < cs.nseg ? tr.seg_end[cs.seg0 + cs.seg] : 0x7fffffff;
+  if (P.ratio_smem) fill_ratios(T, tile, sRatio + (size_t)tid * T.n_powers, cs.idle);
 
-  double* agg = P.out.agg ? P.out.agg + stream * ALERT_AGG_FIELDS : nullptr;
-  if (writer && agg) {
+  const bool has_agg = P.out.agg != nullptr;
+  if (writer && has_agg) {
+    const double* agg = P.out.agg + stream_ll * ALERT_AGG_FIELDS;
     G = TileAgg{};
     G.e = agg[ALERT_AGG_ENERGY]; G.ec = agg[ALERT_AGG_ENERGY_C];
     G.a = agg[ALERT_AGG_ACC]; G.ac = agg[ALERT_AGG_ACC_C];
@@ -214,53 +274,51 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
       G.oe = agg[ALERT_AGG_OR_ENERGY]; G.oec = agg[ALERT_AGG_OR_ENERGY_C];
       G.oa = agg[ALERT_AGG_OR_ACC]; G.oac = agg[ALERT_AGG_OR_ACC_C];
     }
-    open_segment(G, agg, phase);
+    open_segment(G, agg, cs.phase);
   }
-
-  const int kinds = P.kinds;
-  const bool fp64_all = P.flags & ALERT_FLAG_FP64_ALL;
-  const bool no_refine = P.flags & ALERT_FLAG_NO_REFINE;
-  const int* forced = P.out.forced;
 
   // Trace prefetch: the next step's slow-down is copied global -> shared with
   // cp.async (LDGSTS) into one of two per-thread slots, so no register is held
   // across the step and the load latency hides behind a whole step of work.
-  unsigned long long* slot = reinterpret_cast<unsigned long long*>(base + L.slot) + 2 * threadIdx.x;
-  const unsigned slot_sa = (unsigned)__cvta_generic_to_shared(slot);
+  const unsigned slot_sa =
+      (unsigned)__cvta_generic_to_shared(reinterpret_cast<unsigned long long*>(base + L.slot) + 2 * threadIdx.x);
   const bool f64 = tr.slowdown_dtype == ALERT_DTYPE_F64;
   const int esz = f64 ? 8 : 4;
   const char* sptr = static_cast<const char*>(tr.slowdown) +
                      (row * tr.row_stride + (P.step_begin - tr.step_offset) * tr.step_stride) * esz;
-  const long long sinc = tr.step_stride * esz;
   prefetch_s(slot_sa, sptr, f64);
-  const int nsteps = (int)(P.step_end - P.step_begin);
-  for (int i = 0; i < nsteps; ++i) {
-    const long long n = P.step_begin + i;
+  const int n_end = (int)P.step_end;
+  for (int n = (int)P.step_begin; n < n_end; ++n) {
+    const unsigned par = (unsigned)(n - (int)P.step_begin) & 1u;
     asm volatile("cp.async.wait_all;\n" ::: "memory");
-    const unsigned long long s_raw = slot[i & 1];
-    if (i + 1 < nsteps) {
-      sptr += sinc;
-      prefetch_s(slot_sa + 8u * ((i + 1) & 1), sptr, f64);
+    unsigned long long s_raw;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(s_raw) : "r"(slot_sa + 8u * par) : "memory");
+    if (n + 1 < n_end) {
+      sptr += tr.step_stride * esz;
+      prefetch_s(slot_sa + 8u * (par ^ 1u), sptr, f64);
     }
-    if (n >= cur_end && seg + 1 < nseg) {
-      if (agg && writer) flush_segment(G, agg, phase);
-      while (seg + 1 < nseg && n >= cur_end) {
-        ++seg;
-        cur_end = tr.seg_end[seg0 + seg];
-      }
-      phase = tr.seg_phase[seg0 + seg];
-      idle = tr.seg_idle[seg0 + seg];
-      if (ratio_tab) fill_ratios(T, tile, ratio_tab, idle);
-      if (agg && writer) open_segment(G, agg, phase);
+    if (n >= cur_end) {  // segment change (rare): cursor, phase, idle power
+      int seg = cs.seg;
+      const int nseg = cs.nseg;
+      const long long seg0 = cs.seg0;
+      if (has_agg && writer) flush_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase);
+      while (seg + 1 < nseg && n >= tr.seg_end[seg0 + seg]) ++seg;
+      cs.seg = seg;
+      cs.phase = tr.seg_phase[seg0 + seg];
+      cs.idle = tr.seg_idle[seg0 + seg];
+      cur_end = seg + 1 < nseg ? tr.seg_end[seg0 + seg] : 0x7fffffff;
+      if (P.ratio_smem) fill_ratios(T, tile, sRatio + (size_t)tid * T.n_powers, cs.idle);
+      if (has_agg && writer) open_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase);
     }
     // adjust_goal (selector.py:48-70) with group budgets (simulator.py:473-483)
     double goal, period;
+    const int group_size = spec->group_size;
     if (group_size > 0) {
-      if (count == 0) {
-        budget = xmul((double)group_size, spec->t_goal);
-        count = group_size;
+      if (cs.count == 0) {
+        cs.budget = xmul((double)group_size, spec->t_goal);
+        cs.count = group_size;
       }
-      goal = py_max(xsub(xdiv(budget, (double)count), spec->oh), 0.001);
+      goal = py_max(xsub(xdiv(cs.budget, (double)cs.count), spec->oh), 0.001);
       period = xadd(goal, spec->oh);
     } else {
       goal = spec->goal0;
@@ -271,35 +329,44 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
     double s;  // true slow-down of this input: consumed only after the decision
     if (PF == PF_ORACLE) {
       s = s_of_raw(tr, s_raw);
-      d = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, idle, goal, fp64_all);
+      d = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, cs.idle, goal, P.flags & ALERT_FLAG_FP64_ALL);
     } else {
       StepCtx x;
-      make_ctx(x, spec, C64, f.mu, f.sigma2, f.phi, goal, fp64_all);
+      make_ctx(x, spec, C64, f.mu, f.sigma2, f.phi, goal, P.flags & ALERT_FLAG_FP64_ALL);
       x.sv = sv_tile;
       x.has_sv = P.sv_smem;
-      d = alert_decide(T, sA, sB, sCol, tile, x, kinds, no_refine);
+      if (fast && !x.fp64_all) {
+        x.fast = true;
+        x.sF = sF;
+        float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
+        fast_prep(x, tile, fzZ, fzZ + (size_t)n_tiles * n_tdnn, n_tiles, n_tdnn, zpr,
+                  P.fast_rows ? P.zlo + (size_t)si * (n_tdnn + 1) : nullptr);
+      }
+      d = alert_decide<MS>(T, sA, sB, sCol, tile, x, P.kinds, P.flags & ALERT_FLAG_NO_REFINE);
       s = s_of_raw(tr, s_raw);
     }
     int exec_cell = d.cell;
-    if (forced) {
-      const int fc = forced[stream * P.out.stream_stride + n * P.out.step_stride];
+    if (P.out.forced) {
+      const int fc = P.out.forced[stream_ll * P.out.stream_stride + (long long)n * P.out.step_stride];
       if (fc >= 0) exec_cell = T.cell_of_cand[fc];
     }
+    const double idle = cs.idle;
     const Outcome o = execute_measure(sB, C64, spec, exec_cell, s, goal, period, idle);
     if (PF != PF_ORACLE) {  // AlertPolicy.observe, policies.py:105-108
       slowdown_update(P.cfg, f, o.fb_latency, o.fb_t_prof, k_valid);
       const int pw = __float_as_uint(sB[exec_cell].y) >> 20;  // power index from the tie key
-      const double ratio = ratio_tab ? ratio_tab[pw] : py_min(1.0, xdiv(idle, C64[exec_cell].cap));
+      const double ratio = P.ratio_smem ? sRatio[(size_t)tid * T.n_powers + pw]
+                                        : py_min(1.0, xdiv(idle, C64[exec_cell].cap));
       idle_update(P.cfg, f, ratio, ik, P.idle_fix, P.idle_w, P.idle_m);
     }
     if (group_size > 0) {  // simulator.py:501-503
-      budget = xsub(budget, o.latency);
-      count -= 1;
+      cs.budget = xsub(cs.budget, o.latency);
+      cs.count -= 1;
     }
     const AlertOutputs& out = P.out;
     if (writer && out.decision) {
-      const long long oidx = stream * out.stream_stride + n * out.step_stride;
-      out.decision[oidx] = pack_decision(cell_cand(sB[d.cell]), d.level, o, d.refined, phase);
+      const long long oidx = stream_ll * out.stream_stride + (long long)n * out.step_stride;
+      out.decision[oidx] = pack_decision(cell_cand(sB[d.cell]), d.level, o, d.refined, cs.phase);
       if (out.record_dtype == ALERT_DTYPE_F64) {
         if (out.energy) static_cast<double*>(out.energy)[oidx] = o.energy;
         if (out.accuracy) static_cast<double*>(out.accuracy)[oidx] = o.delivered;
@@ -314,7 +381,7 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
         if (out.sigma2) static_cast<float*>(out.sigma2)[oidx] = (float)f.sigma2;
       }
     }
-    if (writer && agg) {  // aggregates in step order (CPython 3.12 sum() semantics)
+    if (writer && has_agg) {  // aggregates in step order (CPython 3.12 sum() semantics)
       neumaier(G.e, G.ec, o.energy);
       neumaier(G.a, G.ac, o.delivered);
       neumaier(G.pe, G.pec, o.energy);
@@ -325,17 +392,17 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
       G.ref += d.refined;
     }
     if (PF == PF_BOTH) {  // OraclePolicy alongside on the same step
-      Decision od = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, idle, goal, fp64_all);
+      Decision od = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, idle, goal, P.flags & ALERT_FLAG_FP64_ALL);
       const Outcome oo = execute_measure(sB, C64, spec, od.cell, s, goal, period, idle);
-      if (writer && agg) {
+      if (writer && has_agg) {
         neumaier(G.oe, G.oec, oo.energy);
         neumaier(G.oa, G.oac, oo.delivered);
         G.ovl += oo.vl; G.ova += oo.va; G.ove += oo.ve;
         G.osame += od.cell == exec_cell;
       }
       if (writer && out.oracle_decision)
-        out.oracle_decision[stream * out.stream_stride + n * out.step_stride] =
-            pack_decision(cell_cand(sB[od.cell]), od.level, oo, false, phase);
+        out.oracle_decision[stream_ll * out.stream_stride + (long long)n * out.step_stride] =
+            pack_decision(cell_cand(sB[od.cell]), od.level, oo, false, cs.phase);
     }
   }
   if (!writer) return;
@@ -346,10 +413,11 @@ __global__ void __launch_bounds__(256, 2) run_kernel(const RunParams P) {
   P.st.innov[stream] = f.innov;
   P.st.phi[stream] = f.phi;
   P.st.m_var[stream] = f.m_var;
-  P.st.group_budget[stream] = budget;
-  P.st.group_count[stream] = count;
-  if (agg) {
-    flush_segment(G, agg, phase);
+  P.st.group_budget[stream] = cs.budget;
+  P.st.group_count[stream] = cs.count;
+  if (has_agg) {
+    double* agg = P.out.agg + stream_ll * ALERT_AGG_FIELDS;
+    flush_segment(G, agg, cs.phase);
     const double steps = (double)(P.step_end - P.step_begin);
     agg[ALERT_AGG_N] += steps;
     agg[ALERT_AGG_ENERGY] = G.e; agg[ALERT_AGG_ENERGY_C] = G.ec;
@@ -442,14 +510,17 @@ inline cudaError_t set_smem(K kern, size_t smem) {
     long long blocks = ((P.stream_end - P.stream_begin) * W + tpb - 1) / tpb;                        \
     cudaError_t e;                                                                                    \
     if (pf == PF_ORACLE) {                                                                            \
-      if ((e = set_smem(run_kernel<W, PF_ORACLE>, smem))) return e;                                   \
-      run_kernel<W, PF_ORACLE><<<(unsigned)blocks, tpb, smem, st>>>(P);                               \
+      if ((e = set_smem(run_kernel<W, PF_ORACLE, MS_ALL>, smem))) return e;                           \
+      run_kernel<W, PF_ORACLE, MS_ALL><<<(unsigned)blocks, tpb, smem, st>>>(P);                       \
     } else if (pf == PF_BOTH) {                                                                       \
-      if ((e = set_smem(run_kernel<W, PF_BOTH>, smem))) return e;                                     \
-      run_kernel<W, PF_BOTH><<<(unsigned)blocks, tpb, smem, st>>>(P);                                 \
+      if ((e = set_smem(run_kernel<W, PF_BOTH, MS_ALL>, smem))) return e;                             \
+      run_kernel<W, PF_BOTH, MS_ALL><<<(unsigned)blocks, tpb, smem, st>>>(P);                         \
+    } else if (P.min_energy_only) {                                                                   \
+      if ((e = set_smem(run_kernel<W, PF_ALERT, MS_MIN_ENERGY>, smem))) return e;                     \
+      run_kernel<W, PF_ALERT, MS_MIN_ENERGY><<<(unsigned)blocks, tpb, smem, st>>>(P);                 \
     } else {                                                                                          \
-      if ((e = set_smem(run_kernel<W, PF_ALERT>, smem))) return e;                                    \
-      run_kernel<W, PF_ALERT><<<(unsigned)blocks, tpb, smem, st>>>(P);                                \
+      if ((e = set_smem(run_kernel<W, PF_ALERT, MS_ALL>, smem))) return e;                            \
+      run_kernel<W, PF_ALERT, MS_ALL><<<(unsigned)blocks, tpb, smem, st>>>(P);                        \
     }                                                                                                 \
     return cudaGetLastError();                                                                        \
   }                                                                                                   \

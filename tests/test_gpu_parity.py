@@ -240,6 +240,52 @@ def test_fp64_all_equals_fast_path():
     np.testing.assert_array_equal(fast.records["energy"], full.records["energy"])
 
 
+def _min_energy_specs(rnd, space, n=8):
+    """Min-energy specs incl. threshold edge cases: q_goal equal to a DNN's
+    accuracy or q_fail, pr_threshold at 1.0 / tiny / unset."""
+    specs = []
+    levels = [d.stages[-1].accuracy for d in space.dnns] + [d.q_fail for d in space.dnns]
+    for k in range(n):
+        q = rnd.choice(levels) if k % 2 else rnd.uniform(0.1, 0.99)
+        pr = [None, rnd.uniform(0.05, 0.99), 1.0 - 1e-12, 1e-12][k % 4]
+        t = rnd.uniform(0.05, 3.0)
+        specs.append(A.ConstraintSpec(mode=A.Mode.MINIMIZE_ENERGY, t_goal=t, q_goal=q, pr_threshold=pr,
+                                      overhead_budget=rnd.choice([0.0, 0.02 * t])))
+    return specs
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fast_scan_equals_full_scan(seed):
+    """The min-energy fast scan (z-thresholds, certified top-2) changes no
+    decision or value against the full FP32 scan (ALERT_FLAG_NO_FAST), for
+    alert / alert-any / alert-trad, any tile width, edge-case goals; and the
+    decisions match the FP64 oracle (teacher forced)."""
+    rnd = random.Random(4242 + seed)
+    space, _, envs = _random_batch(4242 + seed, 36, 160, max_dnns=6, max_powers=6)
+    specs = _min_energy_specs(rnd, space)
+    policy = ["alert", "alert-any", "alert-trad"][seed % 3]
+    try:
+        fast = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64,
+                           lanes_per_stream=[1, 2, 4, 8][seed % 4])
+    except ValueError:
+        pytest.skip("space has no DNN of the policy's kinds")
+    full = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64,
+                       lanes_per_stream=[1, 2, 4, 8][seed % 4], flags=abi.FLAG_NO_FAST)
+    rows = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64,
+                       lanes_per_stream=[1, 2, 4, 8][seed % 4], flags=abi.FLAG_FAST_ROWS)
+    A.get_engine().set_launch(0, 0)
+    np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
+    np.testing.assert_array_equal(rows.decoded()["cand"], full.decoded()["cand"])
+    np.testing.assert_array_equal(rows.records["energy"], full.records["energy"])
+    np.testing.assert_array_equal(fast.records["energy"], full.records["energy"])
+    np.testing.assert_array_equal(fast.agg[:, :abi.AGG_LEVEL0], full.agg[:, :abi.AGG_LEVEL0])
+    for k in range(0, len(envs), 5):
+        rec, _, _ = oracle.run(space, specs[k % len(specs)], envs[k], policy)
+        own = A.run_batch(space, [specs[k % len(specs)]], [envs[k]], policy, records="f64",
+                          trace_dtype=np.float64, forced=rec["cand"][:, None].astype(np.int32))
+        assert_decisions(own.decoded()["cand"][:, 0], rec, f"seed {seed} stream {k}")
+
+
 def test_chunked_steps_bit_identical():
     space, specs, envs = _random_batch(11, 16, 300)
     one = A.run_batch(space, specs, envs, "alert", records="f64", trace_dtype=np.float64)
