@@ -346,6 +346,7 @@ def main():
         "viol_accuracy_rate": float(tot[abi.AGG_VIOL_ACC] / n_all),
         "viol_energy_rate": float(tot[abi.AGG_VIOL_ENERGY] / n_all),
         "fp64_rerank_fraction": float(tot[abi.AGG_REFINED] / n_all),
+        "full_scan_fraction": float(tot[abi.AGG_FULL_SCAN] / n_all),
     }
     if policy == "alert+oracle":
         quality["oracle_mean_energy_j"] = float((tot[abi.AGG_OR_ENERGY] + tot[abi.AGG_OR_ENERGY_C]) / n_all)

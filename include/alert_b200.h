@@ -175,6 +175,7 @@ enum {
   ALERT_AGG_OR_ENERGY_C = 13, ALERT_AGG_OR_ACC = 14, ALERT_AGG_OR_ACC_C = 15,
   ALERT_AGG_OR_VIOL_LAT = 16, ALERT_AGG_OR_VIOL_ACC = 17, ALERT_AGG_OR_VIOL_ENERGY = 18,
   ALERT_AGG_OR_SAME = 19,     /* steps where both chose the same candidate     */
+  ALERT_AGG_FULL_SCAN = 20,   /* min-energy steps the fast scan could not certify (full scan ran) */
   ALERT_AGG_PHASE_BASE = 24,  /* + 8*phase + {n, e, e_c, acc, acc_c, vl, va, ve} */
   ALERT_AGG_PHASE_STRIDE = 8,
   ALERT_AGG_FIELDS = 88

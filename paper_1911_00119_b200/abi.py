@@ -26,6 +26,7 @@ AGG_VIOL_LAT, AGG_VIOL_ACC, AGG_VIOL_ENERGY = 5, 6, 7
 AGG_LEVEL0, AGG_LEVEL1, AGG_LEVEL2, AGG_REFINED = 8, 9, 10, 11
 AGG_OR_ENERGY, AGG_OR_ENERGY_C, AGG_OR_ACC, AGG_OR_ACC_C = 12, 13, 14, 15
 AGG_OR_VIOL_LAT, AGG_OR_VIOL_ACC, AGG_OR_VIOL_ENERGY, AGG_OR_SAME = 16, 17, 18, 19
+AGG_FULL_SCAN = 20  # min-energy steps the fast scan could not certify
 AGG_PHASE_BASE, AGG_PHASE_STRIDE = 24, 8
 AGG_FIELDS = 88
 

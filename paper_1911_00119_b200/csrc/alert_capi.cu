@@ -409,6 +409,10 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   T.phi0 = (1.0 < r) ? 1.0 : r;  // min(1.0, p_idle_prof / max cap), policies.py:90
   T.power_cap64 = reinterpret_cast<const double*>(buf + oPw);
   T.cap_max = (float)max_cap;
+  T.any_mono = 1;  // fast scan's anytime skip (fast_min_energy): stage latencies non-decreasing
+  for (const int2& cd : cols)
+    for (int k = 1; k < cd.y; ++k)
+      if (!(c64[cd.x + k].t >= c64[cd.x + k - 1].t)) T.any_mono = 0;
   tb->buf = buf;
   tb->n_cand = n;
   tb->n_any_cols = (int)cols.size();

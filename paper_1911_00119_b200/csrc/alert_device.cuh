@@ -48,6 +48,7 @@ struct DevTable {
   const int* cell_of_cand;
   const double* power_cap64;  // [n_powers] caps by power index
   double phi0;            // min(1, p_idle_prof / max cap), policies.py:90
+  int any_mono;           // every anytime column's t_prof grows >= 1e-5 relative per stage
   float cap_max;          // largest cap (FP32 error bound of the oracle scan)
 };
 
@@ -341,6 +342,7 @@ struct Decision {
   int cell;
   int level;
   bool refined;
+  bool full = false;  // the min-energy fast scan ran but could not certify
 };
 
 // Level-l objective in FP32: min-energy L0 -> E (relative bound), otherwise -acc.
@@ -532,9 +534,7 @@ __device__ __forceinline__ void cell_pass(const DevTable& T, const float4* __res
 // has a strictly larger FP64 energy and P1 is the reference's choice.
 // Otherwise (near-ties, boundary cells, empty level 0) the full scan runs.
 constexpr float kPenH = 1099511627776.0f;  // 2^40: sign-exact scaling of the penalty
-#ifndef ALERT_FAST_CHUNK
-#define ALERT_FAST_CHUNK 8  // traditional cells in flight per lane (power of two <= 8)
-#endif
+
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
@@ -660,62 +660,136 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
       return pack_key(F.y * fmax3(x.mu_e, fmaf(x.phig, F.x, x.ompmu), fmaf(mgH, F.x, Td)), __float_as_uint(F.w));
     };
     const int n = T.n_trad;
-    constexpr int K = ALERT_FAST_CHUNK;
     int c = lane;
-    for (; c + (K - 1) * W < n; c += K * W) {
+    for (; c + 7 * W < n; c += 8 * W) {
       const float s1 = t.p1;
-      float k[K];
+      float k[8];
 #pragma unroll
-      for (int u = 0; u < K; ++u) k[u] = key_of(sF[c + u * W]);
+      for (int u = 0; u < 8; ++u) k[u] = key_of(sF[c + u * W]);
 #pragma unroll
-      for (int u = 0; u < K; u += 2) t.push2(k[u], k[u + 1]);
+      for (int u = 0; u < 8; u += 2) t.push2(k[u], k[u + 1]);
       if (t.p1 != s1) t.blk = c;
     }
-    if (c < n) {  // < K cells left: the padded table is read past the end, keys masked
-      const float s1 = t.p1;
-      float k[K];
+    // remainder (< 8 cells) in quarter-chunks: positions 0-3 then 4-7 of the
+    // last 8-group (keys carry the staged position, blk the group start)
+    const int c8 = c;
 #pragma unroll
-      for (int u = 0; u < K; ++u) {
-        const float kk = key_of(sF[c + u * W]);
-        k[u] = c + u * W < n ? kk : kInfF;
-      }
-#pragma unroll
-      for (int u = 0; u < K; u += 2) t.push2(k[u], k[u + 1]);
-      if (t.p1 != s1) t.blk = c;
-    }
-  }
-  if (kinds & 2) {
-    const float qloH = x.q_lo * kPenH;
-    auto any_key = [&](const float4& A, float& acc, unsigned idx) {
-      const float pr = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
-      acc = fmaf(pr, A.z, acc);
-      float pen = fmaf(-kPenH, acc, qloH);
-      if (HAS_PR) pen = fmaxf(pen, fmaf(mgH, A.x, x.Tpr));
-      return pack_key(A.y * fmax3(x.mu_e, fmaf(x.phig, A.x, x.ompmu), pen), idx);
-    };
-    if (W == 1) {  // one flat loop over every anytime cell, 4 in flight; A.w >= 0 starts a column
-      float carry = 0.f;
-      for (int c = T.n_trad; c < T.n_cells; c += 4) {
+    for (int h = 0; h < 2; ++h) {
+      if (c < n) {
         const float s1 = t.p1;
         float k[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float4 A = sA[c + u];  // padded table
-          float acc = A.w >= 0.0f ? A.w : carry;
-          const float kk = any_key(A, acc, u);
-          carry = acc;
-          k[u] = c + u < T.n_cells ? kk : kInfF;
+          const float kk = key_of(sF[c + u * W]);  // padded table: reads past the end are masked
+          k[u] = c + u * W < n ? kk : kInfF;
         }
         t.push2(k[0], k[1]);
         t.push2(k[2], k[3]);
-        if (t.p1 != s1) t.blk = c;
+        if (t.p1 != s1) t.blk = c8;
+        c += 4 * W;
       }
-    } else {
-      for (int col = lane; col < T.n_any_cols; col += W) {
-        const int2 cd = sCol[col];
+    }
+  }
+  if (kinds & 2) {
+    // Anytime columns after the traditional cells, with an exact skip: a
+    // stage whose energy-only key is already >= P2 cannot change (P1, P2)
+    // (the penalty only raises a key).  When every column's profiled latency
+    // is non-decreasing with the stage (T.any_mono: the exact energy is then
+    // non-decreasing, the FP32 keys within 4e-6 relative), a column whose
+    // stage-0 key clears P2 by that margin on every lane of the warp is
+    // skipped whole; in the others the Phi chain runs up to the last
+    // stage some lane still needs.  Energies of later stages are rarely
+    // competitive, so this is usually stage 0 of a few columns or nothing.
+    const float qloH = x.q_lo * kPenH;
+    const unsigned am = __activemask();
+    const int rounds = (T.n_any_cols + W - 1) / W;
+    auto ekey = [&](const float4& A, unsigned k) {
+      return pack_key(A.y * fmaxf(x.mu_e, fmaf(x.phig, A.x, x.ompmu)), k);
+    };
+    auto eval = [&](const float4& A, float& acc, unsigned k) {
+      const float pr = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
+      acc = fmaf(pr, A.z, acc);
+      float pen = fmaf(-kPenH, acc, qloH);
+      if (HAS_PR) pen = fmaxf(pen, fmaf(mgH, A.x, x.Tpr));
+      t.push(pack_key(A.y * fmax3(x.mu_e, fmaf(x.phig, A.x, x.ompmu), pen), k));
+    };
+    if (W == 1) {
+      // One lane per stream: windows of 32 anytime cells.  Pass 1 (all cells,
+      // independent): energy-only keys -> cells some lane of the warp needs
+      // (key < P2); extended down to their column start (the Phi chain needs
+      // the earlier stages).  Pass 2: the Phi chain over those cells only.
+      for (int c0 = T.n_trad; c0 < T.n_cells; c0 += 32) {
+        const int nw = min(32, T.n_cells - c0);
+        unsigned m = 0, st = 0;
+#pragma unroll 4
+        for (int u = 0; u < nw; ++u) {
+          const float4 A = sA[c0 + u];
+          m |= (unsigned)(ekey(A, 0u) < t.p2) << u;
+          st |= (unsigned)(A.w >= 0.0f) << u;
+        }
+        m = __reduce_or_sync(am, m);
+        if (!m) continue;
+        // fill each needed cell down to its column start (the Phi chain needs
+        // the earlier stages); a handful of iterations, warp-uniform
+        unsigned need = 0;
+        for (unsigned mm = m; mm;) {
+          const int hb = 31 - __clz(mm);
+          const unsigned below = hb == 31 ? ~0u : (2u << hb) - 1u;
+          const unsigned sb = st & below;
+          const int s0 = sb ? 31 - __clz(sb) : 0;
+          need |= below & ~((1u << s0) - 1u);
+          mm &= (1u << s0) - 1u;
+        }
+        // a window may start inside a column: its carry is rebuilt from the start
+        float acc = 0.f;
+        if (!(st & 1u) && (need & 1u)) {
+          int cs = c0;
+          while (sA[cs].w < 0.0f) --cs;
+          acc = sA[cs].w;
+          for (int c = cs; c < c0; ++c) {
+            const float4 A = sA[c];
+            acc = fmaf(phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s), A.z, acc);
+          }
+        }
+        while (need) {
+          const int u = __ffs(need) - 1;
+          need &= need - 1;
+          const float4 A = sA[c0 + u];
+          if (A.w >= 0.0f) acc = A.w;
+          const float before = t.p1;
+          eval(A, acc, (unsigned)(u & 7));
+          if (t.p1 != before) t.blk = c0 + (u & ~7);
+        }
+      }
+    } else
+    for (int j0 = 0; j0 < rounds; j0 += 32) {
+      const int jn = min(rounds, j0 + 32);
+      unsigned m;
+      if (T.any_mono) {
+        m = 0;
+#pragma unroll 4
+        for (int j = j0; j < jn; ++j) {
+          const int col = lane + j * W;
+          // later stages: exact energy non-decreasing, FP32 keys within 4e-6 relative
+          if (col < T.n_any_cols && ekey(sA[sCol[col].x], 0u) * (1.0f - 4e-6f) < t.p2) m |= 1u << (j - j0);
+        }
+        m = __reduce_or_sync(am, m);
+      } else {
+        m = jn - j0 == 32 ? ~0u : (1u << (jn - j0)) - 1u;
+      }
+      while (m) {
+        const int j = j0 + __ffs(m) - 1;
+        m &= m - 1;
+        const int col = lane + j * W;
+        const int2 cd = col < T.n_any_cols ? sCol[col] : make_int2(0, 0);
+        int need = -1;
+#pragma unroll
+        for (int k = 0; k < ALERT_MAX_STAGES; ++k)
+          if (k < cd.y && ekey(sA[cd.x + k], (unsigned)k) < t.p2) need = k;
+        const int K = __reduce_max_sync(am, need);
         const float s1 = t.p1;
         float acc = sA[cd.x].w;
-        for (int k = 0; k < cd.y; ++k) t.push(any_key(sA[cd.x + k], acc, (unsigned)k));
+        for (int k = 0; k <= K && k < cd.y; ++k) eval(sA[cd.x + k], acc, (unsigned)k);
         if (t.p1 != s1) t.blk = cd.x;
       }
     }
@@ -862,12 +936,16 @@ template <int MODE, bool HAS_PR, bool OUTLINE, class Tile>
 __device__ __forceinline__ Decision alert_decide_t(const DevTable& T, const float4* sA, const float4* sB,
                                                    const int2* sCol, const Tile& tile, StepCtx& x, int kinds,
                                                    bool no_refine) {
+  bool tried = false;
   if (MODE == ALERT_MODE_MIN_ENERGY && x.fast && !x.fp64_all) {
     Decision d{-1, 0, false};
     if (fast_min_energy<HAS_PR>(T, sA, sB, sCol, tile, x, kinds, d)) return d;
+    tried = true;
   }
-  if (OUTLINE) return alert_decide_full_call<MODE, HAS_PR>(T, sA, sB, sCol, tile, x, kinds, no_refine);
-  return alert_decide_full<MODE, HAS_PR>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+  Decision d = OUTLINE ? alert_decide_full_call<MODE, HAS_PR>(T, sA, sB, sCol, tile, x, kinds, no_refine)
+                       : alert_decide_full<MODE, HAS_PR>(T, sA, sB, sCol, tile, x, kinds, no_refine);
+  d.full = tried;
+  return d;
 }
 
 template <int MS = MS_ALL, class Tile>

@@ -113,7 +113,7 @@ struct TileAgg {
   double oe, oec, oa, oac;  // oracle alongside
   int dn, dvl, dva, dve;    // current segment counts
   int l1, l2, ref, osame;   // launch totals
-  int ovl, ova, ove, pad;
+  int ovl, ova, ove, full;
 };
 
 enum { PF_ALERT = 0, PF_ORACLE = 1, PF_BOTH = 2 };  // policy families
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       const bool in = i < T.n_trad;
       const int off = in ? (i / T.n_powers) * n_tiles * (int)sizeof(float) : 0;
       sF[i] = make_float4(in ? T.cellA[i].x : 0.f, in ? T.cellA[i].y : 0.f, __int_as_float(off),
-                          __int_as_float((i / W) & (ALERT_FAST_CHUNK - 1)));
+                          __int_as_float((i / W) & 7));
     }
   __syncthreads();
   const Cell64* C64 = P.c64_smem ? sC64 : T.c64;
@@ -390,6 +390,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       G.dvl += o.vl; G.dva += o.va; G.dve += o.ve;
       G.l1 += d.level == 1; G.l2 += d.level == 2;
       G.ref += d.refined;
+      G.full += d.full;
     }
     if (PF == PF_BOTH) {  // OraclePolicy alongside on the same step
       Decision od = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, idle, goal, P.flags & ALERT_FLAG_FP64_ALL);
@@ -426,6 +427,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
     agg[ALERT_AGG_LEVEL1] += (double)G.l1;
     agg[ALERT_AGG_LEVEL2] += (double)G.l2;
     agg[ALERT_AGG_REFINED] += (double)G.ref;
+    agg[ALERT_AGG_FULL_SCAN] += (double)G.full;
     if (PF == PF_BOTH) {
       agg[ALERT_AGG_OR_ENERGY] = G.oe; agg[ALERT_AGG_OR_ENERGY_C] = G.oec;
       agg[ALERT_AGG_OR_ACC] = G.oa; agg[ALERT_AGG_OR_ACC_C] = G.oac;
