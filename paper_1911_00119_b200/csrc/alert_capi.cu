@@ -510,7 +510,7 @@ static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const 
   SmemLayout L(T.n_cells, T.n_any_cols, tpb / W, P.c64_smem ? T.n_cells : 0, tpb / W,
                P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
                (P.fast_smem && !P.fast_rows) ? T.n_trad / T.n_powers : 0,
-               (P.fast_smem && !P.fast_rows) ? T.n_trad : 0);
+               (P.fast_smem && !P.fast_rows) ? T.n_trad : 0, P.fast_smem && !P.fast_rows);
   return L.total;
 }
 

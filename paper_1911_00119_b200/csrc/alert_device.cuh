@@ -164,6 +164,7 @@ struct StepCtx {
   int tS;
   const float4* sF;  // traditional cells {1/t, cap t, byte offset of the DNN's threshold in tT, 0}
   const float* zrow; // row mode (large tables): the spec's z' per traditional DNN (global, L1)
+  const unsigned* wst;  // per 32-cell window of anytime cells: column-start bits (shared)
   float hs, hm;      // T_d = fma(z'_d, hs, hm)
   float Tpr;     // same for the pr_threshold z-bound (anytime cells)
 };
@@ -187,6 +188,7 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
   x.tS = 0;
   x.sF = nullptr;
   x.zrow = nullptr;
+  x.wst = nullptr;
   x.hs = x.hm = 0.f;
   x.Tpr = -kInfF;
   x.mu = mu;
@@ -594,7 +596,11 @@ __device__ __forceinline__ void fast_prep(StepCtx& x, const Tile& tile, const fl
     x.zrow = zrow;
     return;
   }
-  for (int d = tile.thread_rank(); d < n_tdnn; d += Tile::num_threads()) tT[d * tS] = fmaf(zt[d * tS], x.hs, x.hm);
+  const int step = Tile::num_threads() * tS;
+  const float* zp = zt + tile.thread_rank() * tS;
+  float* tp = tT + tile.thread_rank() * tS;
+  for (int d = tile.thread_rank(); d < n_tdnn; d += Tile::num_threads(), zp += step, tp += step)
+    *tp = fmaf(*zp, x.hs, x.hm);
   x.tT = tT;
   x.tS = tS;
   if (Tile::num_threads() > 1) tile.sync();
@@ -718,17 +724,26 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
       // independent): energy-only keys -> cells some lane of the warp needs
       // (key < P2); extended down to their column start (the Phi chain needs
       // the earlier stages).  Pass 2: the Phi chain over those cells only.
+      // energy-only keys scaled by (1 - 4e-6): below P2 whenever the packed
+      // key could be (truncation <= 7 ulp, FP32 rounding of the scaling)
+      const float sc = 1.0f - 4e-6f;
+      const float mu_es = x.mu_e * sc, phigs = x.phig * sc, ompmus = x.ompmu * sc;
       for (int c0 = T.n_trad; c0 < T.n_cells; c0 += 32) {
         const int nw = min(32, T.n_cells - c0);
-        unsigned m = 0, st = 0;
-#pragma unroll 4
-        for (int u = 0; u < nw; ++u) {
-          const float4 A = sA[c0 + u];
-          m |= (unsigned)(ekey(A, 0u) < t.p2) << u;
-          st |= (unsigned)(A.w >= 0.0f) << u;
+        unsigned m = 0;
+        for (int ub = 0; ub < nw; ub += 8) {
+          unsigned b = 0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 A = sA[c0 + ub + u];  // padded table; bits past the end are cleared below
+            if (A.y * fmaxf(mu_es, fmaf(phigs, A.x, ompmus)) < t.p2) b |= 1u << u;
+          }
+          m |= b << ub;
         }
+        if (nw < 32) m &= (1u << nw) - 1u;
         m = __reduce_or_sync(am, m);
         if (!m) continue;
+        const unsigned st = x.wst[(c0 - T.n_trad) >> 5];  // column starts in this window
         // fill each needed cell down to its column start (the Phi chain needs
         // the earlier stages); a handful of iterations, warp-uniform
         unsigned need = 0;

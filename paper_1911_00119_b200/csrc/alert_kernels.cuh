@@ -52,13 +52,14 @@ struct ColdState {
 
 // Shared-memory layout of run_kernel (host and device compute it identically).
 struct SmemLayout {
-  size_t B, col, spec, c64, ratio, agg, sv, fz, ff, cold, slot, total;
+  size_t B, col, spec, c64, ratio, agg, sv, fz, ff, wst, cold, slot, total;
   __host__ __device__ static size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
   // pad = look-ahead rows past the end of the cell / column tables for a tile
   // width W: 2 chunks of 4 cells (see cell_pass), so 8 W + 8.
   __host__ __device__ static int pad_rows(int W) { return 8 * W + 8; }
   __host__ __device__ SmemLayout(int n_cells, int n_cols, int n_spec, int n_c64, int n_tiles, int n_ratio,
-                                 size_t agg_bytes, int n_sv, int W, int n_fz = 0, int n_ff = 0) {
+                                 size_t agg_bytes, int n_sv, int W, int n_fz = 0, int n_ff = 0,
+                                 bool flat = false) {
     B = sizeof(float4) * (size_t)(n_cells + pad_rows(W));
     col = B + sizeof(float4) * (size_t)n_cells;
     spec = up16(col + sizeof(int2) * (size_t)(n_cols + pad_rows(W)));
@@ -68,7 +69,8 @@ struct SmemLayout {
     sv = up16(agg + agg_bytes * (size_t)n_tiles);
     fz = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);  // 2 x [n_fz][n_tiles]: Z, T
     ff = up16(fz + 2 * sizeof(float) * (size_t)n_tiles * (size_t)n_fz);  // fast-scan traditional cells
-    cold = up16(ff + (n_ff ? sizeof(float4) * (size_t)(n_ff + pad_rows(W)) : 0));
+    wst = up16(ff + (flat ? sizeof(float4) * (size_t)(n_ff + pad_rows(W)) : 0));
+    cold = up16(wst + (flat ? sizeof(unsigned) * (size_t)(n_cells / 32 + 2) : 0));
     slot = up16(cold + sizeof(ColdState) * (size_t)n_tiles * (size_t)W);
     total = up16(slot + 16 * (size_t)n_tiles * (size_t)W);  // two 8-byte trace slots per thread
   }
@@ -169,7 +171,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   const int n_tdnn = T.n_trad / T.n_powers;
   const SmemLayout L(T.n_cells, T.n_any_cols, n_tiles, P.c64_smem ? T.n_cells : 0, n_tiles,
                      P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
-                     (P.zlo && !P.fast_rows) ? n_tdnn : 0, (P.zlo && !P.fast_rows) ? T.n_trad : 0);
+                     (P.zlo && !P.fast_rows) ? n_tdnn : 0, (P.zlo && !P.fast_rows) ? T.n_trad : 0,
+                     P.zlo && !P.fast_rows);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
   float4* sB = reinterpret_cast<float4*>(base + L.B);
@@ -190,6 +193,14 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       const int off = in ? (i / T.n_powers) * n_tiles * (int)sizeof(float) : 0;
       sF[i] = make_float4(in ? T.cellA[i].x : 0.f, in ? T.cellA[i].y : 0.f, __int_as_float(off),
                           __int_as_float((i / W) & 7));
+    }
+  unsigned* sWst = reinterpret_cast<unsigned*>(base + L.wst);
+  if (P.zlo && !P.fast_rows)  // column-start bits of the anytime cells, per 32-cell window
+    for (int w = threadIdx.x; w * 32 < T.n_cells - T.n_trad; w += blockDim.x) {
+      unsigned b = 0;
+      for (int u = 0; u < 32 && T.n_trad + w * 32 + u < T.n_cells; ++u)
+        b |= (unsigned)(T.cellA[T.n_trad + w * 32 + u].w >= 0.0f) << u;
+      sWst[w] = b;
     }
   __syncthreads();
   const Cell64* C64 = P.c64_smem ? sC64 : T.c64;
@@ -338,6 +349,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       if (fast && !x.fp64_all) {
         x.fast = true;
         x.sF = sF;
+        x.wst = sWst;
         float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
         fast_prep(x, tile, fzZ, fzZ + (size_t)n_tiles * n_tdnn, n_tiles, n_tdnn, zpr,
                   P.fast_rows ? P.zlo + (size_t)si * (n_tdnn + 1) : nullptr);

@@ -397,6 +397,8 @@ def test_oracle_fp32_scan_equals_fp64(seed):
                            flags=abi.FLAG_FP64_ALL)
         np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
         np.testing.assert_array_equal(fast.agg[:, :abi.AGG_REFINED], full.agg[:, :abi.AGG_REFINED])
-        np.testing.assert_array_equal(fast.agg[:, abi.AGG_OR_ENERGY:], full.agg[:, abi.AGG_OR_ENERGY:])
+        np.testing.assert_array_equal(fast.agg[:, abi.AGG_OR_ENERGY:abi.AGG_FULL_SCAN],
+                                      full.agg[:, abi.AGG_OR_ENERGY:abi.AGG_FULL_SCAN])  # FULL_SCAN: path counter
+        np.testing.assert_array_equal(fast.agg[:, abi.AGG_PHASE_BASE:], full.agg[:, abi.AGG_PHASE_BASE:])
         if policy == "alert+oracle":
             np.testing.assert_array_equal(fast.oracle_decision & 0xFFFF, full.oracle_decision & 0xFFFF)
