@@ -61,8 +61,13 @@ enum {                                                            /* policies.py
   ALERT_POLICY_ALERT_ANY = 1,   /* "alert-any"  (anytime DNNs only)           */
   ALERT_POLICY_ALERT_TRAD = 2,  /* "alert-trad" (traditional DNNs only)       */
   ALERT_POLICY_ORACLE = 3,      /* "oracle" (clairvoyant per-input optimum)   */
-  ALERT_POLICY_ALERT_WITH_ORACLE = 4 /* ALERT executed, oracle evaluated alongside
+  ALERT_POLICY_ALERT_WITH_ORACLE = 4, /* ALERT executed, oracle evaluated alongside
                                         on the same step (config 5 fused path) */
+  /* comparison schemes (policies.py:211-454) */
+  ALERT_POLICY_ORACLE_STATIC = 5, /* "oracle-static": best fixed candidate over the whole trace */
+  ALERT_POLICY_SYS_ONLY = 6,      /* "sys-only": fastest traditional DNN, power cap adapted    */
+  ALERT_POLICY_APP_ONLY = 7,      /* "app-only": one anytime DNN at max power, stage adapted   */
+  ALERT_POLICY_NO_COORD = 8       /* "no-coord": stage and power controllers uncoordinated     */
 };
 enum { ALERT_DTYPE_F32 = 0, ALERT_DTYPE_F64 = 1 };
 
@@ -90,6 +95,12 @@ typedef struct AlertSpaceDesc {
   const double* stage_t_prof;    /* [total_stages][n_powers] seconds           */
   const double* power_cap;       /* [n_powers] PowerSetting.cap_watts          */
   double p_idle_prof;            /* ConfigSpace.p_idle_prof                    */
+  /* DNNs of the comparison schemes, chosen by the host from the DnnProfile ids
+   * (the ABI carries no ids): sys-only = fastest_dnn(space, last power,
+   * TRADITIONAL) (policies.py:292, model.py:166-176); app-only / no-coord =
+   * _pick_anytime (policies.py:324-329).  -1 = no such DNN. */
+  int32_t sys_dnn;
+  int32_t app_dnn;
 } AlertSpaceDesc;
 
 /* Filter constants: KalmanConfig (estimator.py:18-30) + IdleFilterConfig (:87-91). */
@@ -159,6 +170,10 @@ typedef struct AlertState {
   double* m_var;
   double* group_budget;
   int32_t* group_count;
+  /* per-stream state of the comparison schemes (NULL allowed for the others):
+   * oracle-static = chosen candidate, no-coord = stage | power << 8;
+   * -1 = not begun (the run performs begin()) */
+  int32_t* policy_aux;
 } AlertState;
 
 /* Per-stream FP64 aggregate block (in/out, accumulated in step order).  The

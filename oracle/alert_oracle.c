@@ -509,6 +509,91 @@ static void neumaier(double* s, double* c, double x) {
   *s = t;
 }
 
+/* index of (dnn i, power j, target) in the candidate enumeration
+ * (policies.py:59-67 _configs order) */
+static int cand_index(const Space* s, int i, int j, int target) {
+  const AlertSpaceDesc* d = s->d;
+  int c = 0;
+  for (int k = 0; k < i; ++k)
+    c += d->n_powers * (d->dnn_kind[k] == ALERT_KIND_TRADITIONAL ? 1 : d->dnn_n_stages[k]);
+  if (d->dnn_kind[i] == ALERT_KIND_TRADITIONAL) return c + j;
+  return c + j * d->dnn_n_stages[i] + (target - 1);
+}
+
+/* OracleStaticPolicy.begin (policies.py:221-265): best fixed candidate over
+ * the realized trace; tot_energy / tot_acc are plain running sums. */
+static int oracle_static_choice(const Space* s, const AlertSpec* spec, int64_t n, const double* sd,
+                                const double* idle) {
+  const AlertSpaceDesc* d = s->d;
+  double t_goal = spec->t_goal - spec->overhead_budget;
+  int best = -1, bel = 0, bi = 0, bj = 0, bt = 0;
+  double bo = 0.0, bv = 0.0;
+  int c = 0;
+  for (int i = 0; i < d->n_dnns; ++i) {
+    int trad = d->dnn_kind[i] == ALERT_KIND_TRADITIONAL;
+    int nt = trad ? 1 : d->dnn_n_stages[i];
+    for (int j = 0; j < d->n_powers; ++j)
+      for (int tk = 0; tk < nt; ++tk, ++c) {
+        int target = trad ? 0 : tk + 1;
+        int64_t lv = 0, av = 0, ev = 0;
+        double te = 0.0, ta = 0.0;
+        for (int64_t k = 0; k < n; ++k) {
+          Exact x = exact_eval(s, spec, sd[k], idle[k], i, j, target, t_goal);
+          lv += !x.met;
+          if (spec->mode == ALERT_MODE_MIN_ENERGY) av += x.delivered < spec->q_goal;
+          else ev += x.energy > spec->e_goal;
+          te += x.energy;
+          ta += x.delivered;
+        }
+        double mean_obj = spec->mode == ALERT_MODE_MIN_ENERGY ? te / (double)n : -ta / (double)n;
+        int64_t mx = lv > av ? lv : av;
+        if (ev > mx) mx = ev;
+        int eligible = (double)mx <= 0.10 * (double)n;
+        double tv = (double)(lv + av + ev);
+        /* key = (0, mean_obj, total_viol, j, i, t) if eligible else (1, total_viol, mean_obj, j, i, t) */
+        double k1 = eligible ? mean_obj : tv, k2 = eligible ? tv : mean_obj;
+        int less;
+        if (best < 0) less = 1;
+        else if (!eligible != !bel) less = eligible;
+        else if (k1 != bo) less = k1 < bo;
+        else if (k2 != bv) less = k2 < bv;
+        else if (j != bj) less = j < bj;
+        else if (i != bi) less = i < bi;
+        else less = target < bt;
+        if (less) {
+          best = c; bel = eligible; bo = k1; bv = k2; bi = i; bj = j; bt = target;
+        }
+      }
+  }
+  return best;
+}
+
+/* SysOnlyPolicy.decide (policies.py:298-313): cheapest cap predicted on time */
+static int sys_only_power(const Space* s, const OracleEst* est, const OracleIdle* idl, int dnn, int stage0,
+                          double goal) {
+  const AlertSpaceDesc* d = s->d;
+  int bj = -1;
+  double be = 0.0;
+  for (int j = 0; j < d->n_powers; ++j) {
+    double t = t_prof_of(s, dnn, stage0, j);
+    if (est->mu * t > goal) continue;
+    double e = oracle_energy_mean(est, idl, d->power_cap[j], t, goal);
+    if (bj < 0 || e < be) { be = e; bj = j; }
+  }
+  return bj < 0 ? d->n_powers - 1 : bj;
+}
+
+/* AppOnlyPolicy.decide (policies.py:350-356): best expected-accuracy stage */
+static int app_only_stage(const Space* s, const OracleEst* est, int dnn, int power, double goal) {
+  int best = 1;
+  double ba = -1.0;
+  for (int k = 1; k <= s->d->dnn_n_stages[dnn]; ++k) {
+    double acc = anytime_acc(s, est, dnn, power, k, goal);
+    if (acc > ba) { best = k; ba = acc; }
+  }
+  return best;
+}
+
 static int kinds_for(int policy) {
   if (policy == ALERT_POLICY_ALERT_ANY) return 1 << ALERT_KIND_ANYTIME;
   if (policy == ALERT_POLICY_ALERT_TRAD) return 1 << ALERT_KIND_TRADITIONAL;
@@ -526,6 +611,11 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
   int any = 0;
   for (int i = 0; i < d->n_dnns; ++i) any |= (kinds >> d->dnn_kind[i]) & 1;
   if (!any) return ALERT_ERR_NO_CANDIDATE;
+  const int baseline = policy >= ALERT_POLICY_ORACLE_STATIC;
+  if ((policy == ALERT_POLICY_SYS_ONLY && d->sys_dnn < 0) ||
+      ((policy == ALERT_POLICY_APP_ONLY || policy == ALERT_POLICY_NO_COORD) && d->app_dnn < 0))
+    return ALERT_ERR_NO_CANDIDATE;
+  int32_t aux = -1;  /* oracle-static: candidate; no-coord: stage | power << 8 */
   OracleEst est;
   OracleIdle idl;
   double budget = 0.0;
@@ -534,11 +624,15 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
     est.mu = state[0]; est.sigma2 = state[1]; est.k_gain = state[2]; est.q_noise = state[3];
     est.innov = state[4]; idl.phi = state[5]; idl.m_var = state[6];
     budget = state[7]; count = (int32_t)state[8];
+    aux = (int32_t)state[9];
   } else {
     oracle_slowdown_init(cfg, &est);
     idl.phi = py_min(1.0, d->p_idle_prof / d->power_cap[d->n_powers - 1]);
     idl.m_var = cfg->m0;
   }
+  if (aux < 0 && policy == ALERT_POLICY_ORACLE_STATIC) aux = oracle_static_choice(s, spec, n_steps, sd, idle);
+  if (aux < 0 && policy == ALERT_POLICY_NO_COORD)
+    aux = d->dnn_n_stages[d->app_dnn] | ((d->n_powers - 1) << 8); /* policies.py:385-386 */
   int has_group = spec->group_size > 0;
   for (int64_t n = 0; n < n_steps; ++n) {
     if (has_group && count == 0) { /* simulator.py:473-478 */
@@ -554,6 +648,22 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
     int32_t or_level = 0;
     if (policy == ALERT_POLICY_ORACLE) {
       cand = oracle_decide_s(s, spec, sd[n], idle[n], goal, &level, &gap);
+    } else if (policy == ALERT_POLICY_ORACLE_STATIC) {
+      cand = aux; /* OracleStaticPolicy.decide, policies.py:268-269 */
+    } else if (policy == ALERT_POLICY_SYS_ONLY) {
+      cand = cand_index(s, d->sys_dnn, sys_only_power(s, &est, &idl, d->sys_dnn, 0, goal), 0);
+    } else if (policy == ALERT_POLICY_APP_ONLY) {
+      int pj = d->n_powers - 1;
+      cand = cand_index(s, d->app_dnn, pj, app_only_stage(s, &est, d->app_dnn, pj, goal));
+    } else if (policy == ALERT_POLICY_NO_COORD) {
+      /* NoCoordPolicy.decide (policies.py:392-428): the stage for the old
+       * power, the power for the old stage, both from the same feedback (the
+       * two estimators receive identical updates, so one is kept) */
+      int st_old = aux & 0xff, pj_old = aux >> 8;
+      int st = app_only_stage(s, &est, d->app_dnn, pj_old, goal);
+      int pj = sys_only_power(s, &est, &idl, d->app_dnn, st_old - 1, goal);
+      aux = st | (pj << 8);
+      cand = cand_index(s, d->app_dnn, pj, st);
     } else {
       int np = predict_all_s(s, &est, &idl, spec, goal, preds);
       cand = select_s(s, preds, np, spec, kinds, &level, &gap, &boundary);
@@ -566,10 +676,12 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
     oracle_candidate(d, exec_c, &di, &pj, &tg);
     Exec o = execute_decision(s, sd[n], di, pj, tg, goal);
     Meas m = measure(s, spec, di, pj, &o, idle[n], period);
-    /* AlertPolicy.observe, policies.py:105-108 (oracle: no-op, :207-208) */
-    if (policy != ALERT_POLICY_ORACLE) {
+    /* AlertPolicy.observe, policies.py:105-108 (oracle: no-op, :207-208);
+     * sys-only / no-coord :315-318 / :430-439; app-only slow-down only :359-360 */
+    if (policy != ALERT_POLICY_ORACLE && policy != ALERT_POLICY_ORACLE_STATIC) {
       if (oracle_slowdown_update(cfg, &est, o.fb_latency, o.fb_t_prof)) return ALERT_ERR_INVALID_TRACE;
-      if (oracle_idle_update(cfg, &idl, idle[n], d->power_cap[pj])) return ALERT_ERR_INVALID_TRACE;
+      if (policy != ALERT_POLICY_APP_ONLY && oracle_idle_update(cfg, &idl, idle[n], d->power_cap[pj]))
+        return ALERT_ERR_INVALID_TRACE;
     }
     if (has_group) { /* simulator.py:501-503 */
       budget -= m.latency;
@@ -621,7 +733,9 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
     state[0] = est.mu; state[1] = est.sigma2; state[2] = est.k_gain; state[3] = est.q_noise;
     state[4] = est.innov; state[5] = idl.phi; state[6] = idl.m_var;
     state[7] = budget; state[8] = (double)count;
+    state[9] = (double)aux;
   }
+  (void)baseline;
   return 0;
 }
 
@@ -686,7 +800,7 @@ static void* batch_worker(void* arg) {
       ph[n] = t->seg_phase[row * t->max_segments + seg];
     }
     int32_t si = J->stream_spec ? J->stream_spec[k] : (int32_t)(k % J->n_specs);
-    double* st = J->state ? J->state + 9 * k : NULL;
+    double* st = J->state ? J->state + ORACLE_STATE_FIELDS * k : NULL;
     int r = run_s(&s, &J->specs[si], J->cfg, J->policy, len, sd, idle, ph, NULL, NULL,
                   J->agg + (size_t)ALERT_AGG_FIELDS * k, st, J->step_begin > 0, preds);
     if (r) J->status = r;

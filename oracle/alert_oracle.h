@@ -28,6 +28,8 @@ typedef struct OracleIdle {  /* IdlePowerEstimate, estimator.py:94-98 */
   double phi, m_var;
 } OracleIdle;
 
+#define ORACLE_STATE_FIELDS 10
+
 /* One StepRecord (simulator.py:311-326) plus the policy state after observe
  * and near-tie diagnostics (top-2 relative gap of the primary objective at the
  * chosen fallback level; minimum relative constraint-boundary distance). */
@@ -76,7 +78,8 @@ int oracle_oracle_decide(const AlertSpaceDesc* sp, const AlertSpec* spec, double
  * (s, idle power, phase id) for one stream.  policy = ALERT_POLICY_*.
  * forced[n] >= 0 executes that candidate instead (teacher forcing).
  * rec (nullable) gets n_steps records; agg (nullable) ALERT_AGG_FIELDS sums;
- * state (nullable, in/out, 9 doubles: mu sigma2 k q y phi m budget count) —
+ * state (nullable, in/out, ORACLE_STATE_FIELDS doubles: mu sigma2 k q y phi m
+ * budget count aux; aux = AlertState.policy_aux of the comparison schemes) —
  * when state_in is nonzero the run resumes from it instead of begin(). */
 int oracle_run(const AlertSpaceDesc* sp, const AlertSpec* spec, const AlertFilterConfig* cfg,
                int policy, int64_t n_steps, const double* s, const double* idle,
@@ -85,7 +88,7 @@ int oracle_run(const AlertSpaceDesc* sp, const AlertSpec* spec, const AlertFilte
 
 /* Batched runs over a HOST AlertTrace (same layout as the device one) with
  * n_threads POSIX threads, one stream at a time per thread.  agg:
- * [n_streams][ALERT_AGG_FIELDS]; state: [n_streams][9] (nullable). */
+ * [n_streams][ALERT_AGG_FIELDS]; state: [n_streams][ORACLE_STATE_FIELDS] (nullable). */
 int oracle_run_batch(const AlertSpaceDesc* sp, const AlertSpec* specs, int32_t n_specs,
                      const int32_t* stream_spec, const AlertFilterConfig* cfg, int policy,
                      const AlertTrace* trace, int64_t n_streams, int64_t step_begin, int64_t step_end,

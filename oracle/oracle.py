@@ -20,6 +20,7 @@ from paper_1911_00119_b200.packing import filter_config, pack_space, pack_specs,
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "liboracle.so"
+STATE_FIELDS = 10  # ORACLE_STATE_FIELDS: mu sigma2 k q y phi m budget count aux
 
 RECORD_DTYPE = np.dtype(
     [(n, "<i4") for n in ("cand", "dnn", "power", "stage", "level", "completed", "met", "phase",
@@ -113,7 +114,7 @@ def run(space, spec, env, policy: str = "alert", kalman=None, forced=None, group
     f = None if forced is None else np.ascontiguousarray(forced, dtype=np.int32)
     records = np.zeros(n, RECORD_DTYPE)
     agg = np.zeros(abi.AGG_FIELDS, np.float64)
-    st = np.zeros(9, np.float64) if state is None else np.array(state, np.float64)
+    st = np.zeros(STATE_FIELDS, np.float64) if state is None else np.array(state, np.float64)
     cfg = filter_config(kalman)
     sp = spec_struct(rec)
     r = lib().oracle_run(C.byref(ps.desc), C.byref(sp), C.byref(cfg), policy_code(policy), n,
@@ -202,7 +203,7 @@ def run_batch(space, spec_records, packed_envs, n_streams, policy="alert", kalma
     tr, keep = host_trace_struct(packed_envs, stream_row)
     ss = None if stream_spec is None else np.ascontiguousarray(stream_spec, np.int32)
     agg = np.zeros((n_streams, abi.AGG_FIELDS), np.float64)
-    st = np.zeros((n_streams, 9), np.float64) if state is None else state
+    st = np.zeros((n_streams, STATE_FIELDS), np.float64) if state is None else state
     end = packed_envs.n_steps if step_end is None else step_end
     cfg = filter_config(kalman)
     r = lib().oracle_run_batch(C.byref(ps.desc), _p(specs), len(specs), _p(ss), C.byref(cfg),

@@ -12,6 +12,8 @@ KIND_TRADITIONAL, KIND_ANYTIME = 0, 1
 MODE_MIN_ENERGY, MODE_MAX_ACCURACY = 0, 1
 LEVEL_NONE, LEVEL_DROPPED_ENERGY, LEVEL_DROPPED_ACCURACY = 0, 1, 2
 POLICY_ALERT, POLICY_ALERT_ANY, POLICY_ALERT_TRAD, POLICY_ORACLE, POLICY_ALERT_WITH_ORACLE = range(5)
+# comparison schemes (policies.py:211-454)
+POLICY_ORACLE_STATIC, POLICY_SYS_ONLY, POLICY_APP_ONLY, POLICY_NO_COORD = range(5, 9)
 DTYPE_F32, DTYPE_F64 = 0, 1
 FLAG_FP64_ALL = 0x1
 FLAG_NO_REFINE = 0x2
@@ -59,6 +61,7 @@ class AlertSpaceDesc(C.Structure):
         ("dnn_kind", _ip), ("dnn_n_stages", _ip), ("dnn_q_fail", _dp),
         ("stage_accuracy", _dp), ("stage_t_prof", _dp), ("power_cap", _dp),
         ("p_idle_prof", C.c_double),
+        ("sys_dnn", C.c_int32), ("app_dnn", C.c_int32),
     ]
 
 
@@ -105,6 +108,7 @@ class AlertState(C.Structure):
         ("mu", C.c_void_p), ("sigma2", C.c_void_p), ("k_gain", C.c_void_p),
         ("q_noise", C.c_void_p), ("innov", C.c_void_p), ("phi", C.c_void_p),
         ("m_var", C.c_void_p), ("group_budget", C.c_void_p), ("group_count", C.c_void_p),
+        ("policy_aux", C.c_void_p),
     ]
 
 

@@ -77,8 +77,24 @@ def pack_space(space, check: bool = True) -> PackedSpace:
         dnn_q_fail=_ptr(q_fail, C.c_double), stage_accuracy=_ptr(acc, C.c_double),
         stage_t_prof=_ptr(arrays["t_prof"], C.c_double), power_cap=_ptr(caps, C.c_double),
         p_idle_prof=float(space.p_idle_prof),
+        sys_dnn=baseline_dnns(space)[0], app_dnn=baseline_dnns(space)[1],
     )
     return PackedSpace(desc, arrays, cands, space)
+
+
+def baseline_dnns(space) -> tuple[int, int]:
+    """DNN indices of the comparison schemes (-1 = none): sys-only runs
+    fastest_dnn(space, last power, TRADITIONAL) (policies.py:292,
+    model.py:166-176: minimal final-stage latency, ties to the lower id);
+    app-only / no-coord run _pick_anytime (policies.py:324-329: most stages,
+    ties to the higher id)."""
+    dnns = list(space.dnns)
+    last = len(space.powers) - 1
+    trad = [k for k, d in enumerate(dnns) if kind_of(d) is DnnKind.TRADITIONAL]
+    anyt = [k for k, d in enumerate(dnns) if kind_of(d) is DnnKind.ANYTIME]
+    sys_dnn = min(trad, key=lambda k: (dnns[k].stages[-1].t_prof[last], dnns[k].id)) if trad else -1
+    app_dnn = max(anyt, key=lambda k: (len(dnns[k].stages), dnns[k].id)) if anyt else -1
+    return sys_dnn, app_dnn
 
 
 def z_quantile(p: float) -> float:
@@ -133,7 +149,8 @@ def filter_config(kalman: KalmanConfig | None = None,
 def policy_code(name: str) -> int:
     codes = {"alert": abi.POLICY_ALERT, "alert-any": abi.POLICY_ALERT_ANY,
              "alert-trad": abi.POLICY_ALERT_TRAD, "oracle": abi.POLICY_ORACLE,
-             "alert+oracle": abi.POLICY_ALERT_WITH_ORACLE}
+             "alert+oracle": abi.POLICY_ALERT_WITH_ORACLE, "oracle-static": abi.POLICY_ORACLE_STATIC,
+             "sys-only": abi.POLICY_SYS_ONLY, "app-only": abi.POLICY_APP_ONLY, "no-coord": abi.POLICY_NO_COORD}
     if name not in codes:
         raise ValueError(f"unknown policy {name!r}; choose from {tuple(codes)}")
     return codes[name]

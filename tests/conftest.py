@@ -23,3 +23,9 @@ def golden_runs():
 def golden_predict():
     from helpers import load_golden_predict
     return load_golden_predict()
+
+
+@pytest.fixture(scope="session")
+def golden_baselines():
+    from helpers import load_golden_runs
+    return load_golden_runs("golden_baselines.npz")

@@ -2,7 +2,10 @@
 
 Run in the build container, where /root/reference exists:
     python tests/golden/make_golden.py
-Writes tests/golden/golden_runs.npz and tests/golden/golden_predict.npz.
+Writes tests/golden/golden_runs.npz and tests/golden/golden_predict.npz;
+    python tests/golden/make_golden.py --baselines
+writes tests/golden/golden_baselines.npz (the comparison schemes
+oracle-static / sys-only / app-only / no-coord).
 The reference is imported read-only from /root/reference/pkg/src; nothing at
 test time reads /root/reference — only these committed fixtures.
 """
@@ -65,9 +68,12 @@ class Recording:
 
     def observe(self, record):
         self.inner.observe(record)
-        if isinstance(self.inner, AlertPolicy):
-            e, i = self.inner.est, self.inner.idle
-            self.states.append((e.mu, e.sigma2, e.k_gain, e.q_noise, e.last_innovation, i.phi, i.m_var))
+        inner = self.inner
+        e = getattr(inner, "est", None) or getattr(inner, "est_app", None)
+        i = getattr(inner, "idle", None) or getattr(inner, "idle_sys", None)
+        if e is not None:
+            ip = (i.phi, i.m_var) if i is not None else (np.nan, np.nan)
+            self.states.append((e.mu, e.sigma2, e.k_gain, e.q_noise, e.last_innovation) + ip)
         else:
             self.states.append((np.nan,) * 7)
 
@@ -233,5 +239,57 @@ def main():
     np.savez_compressed(OUT / "golden_predict.npz", **parr)
 
 
+def baselines():
+    """Golden runs of the comparison schemes (policies.py:211-454)."""
+    cases = []
+    space = preset_space()
+    ref = reference_latency(space)
+    tr600 = preset_trace()
+    c1 = ConstraintSpec(mode=Mode.MINIMIZE_ENERGY, t_goal=0.14, q_goal=0.68, overhead_budget=0.01 * ref)
+    tmax = 0.8 * ref
+    cmax = ConstraintSpec(mode=Mode.MAXIMIZE_ACCURACY, t_goal=tmax, e_goal=0.6 * 50.0 * tmax,
+                          pr_threshold=0.95, overhead_budget=0.01 * ref)
+    pols = ("oracle-static", "sys-only", "app-only", "no-coord")
+    for pol in pols:
+        cases.append((f"preset600_minE_{pol}", space, c1, tr600, pol, None))
+        cases.append((f"preset600_maxA_pr95_{pol}", space, cmax, tr600, pol, None))
+    for dm in (0.4, 1.0, 2.0):
+        sp = ConstraintSpec(mode=Mode.MINIMIZE_ENERGY, t_goal=dm * ref, q_goal=0.85, overhead_budget=0.01 * ref)
+        for pol in pols:
+            cases.append((f"preset300_dm{dm}_{pol}", space, sp, preset_trace(phase_length=100), pol, None))
+    trg = replace(preset_trace(phase_length=40), group_size=4)
+    for pol in pols:
+        cases.append((f"group4_minE_{pol}", space, c1, trg, pol, None))
+    cases.append(("kalman_variant_no-coord", space, c1, preset_trace(phase_length=50), "no-coord",
+                  KalmanConfig(q0=0.02, r=0.01, alpha=0.5, sigma2_uses_current_gain=True)))
+    rnd = random.Random(5150)
+    k = 0
+    while len(cases) < 60:
+        rs = random_space(rnd)
+        spc = random_spec(rnd)
+        spc = replace(spc, overhead_budget=rnd.choice([0.0, 0.01 * spc.t_goal]))
+        tr = random_trace(rnd, 60)
+        pol = pols[k % 4]
+        k += 1
+        has_t = any(d.kind is DnnKind.TRADITIONAL for d in rs.dnns)
+        has_a = any(d.kind is DnnKind.ANYTIME for d in rs.dnns)
+        if (pol == "sys-only" and not has_t) or (pol in ("app-only", "no-coord") and not has_a):
+            continue
+        cases.append((f"random{k:02d}_{pol}", rs, spc, tr, pol, None))
+    arrays, meta = {}, []
+    for name, sp, spec, tr, pol, kal in cases:
+        out = run_case(sp, spec, tr, pol, kal)
+        for key, val in out.items():
+            arrays[f"{name}/{key}"] = val
+        meta.append({"name": name, "space": space_to_dict(sp), "spec": spec_json(spec, tr.group_size),
+                     "policy": pol, "kalman": kalman_json(kal), "n_phases": len(tr.phases)})
+        print(name, "E", out["summary"][0], "acc", out["summary"][1])
+    arrays["meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+    np.savez_compressed(OUT / "golden_baselines.npz", **arrays)
+
+
 if __name__ == "__main__":
-    main()
+    if "--baselines" in sys.argv:
+        baselines()
+    else:
+        main()

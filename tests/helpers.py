@@ -54,8 +54,8 @@ class GoldenCase:
         return TrueEnvironment(self.z["s"], self.z["idle"], self.z["phase"])
 
 
-def load_golden_runs():
-    z = np.load(GOLDEN / "golden_runs.npz")
+def load_golden_runs(name: str = "golden_runs.npz"):
+    z = np.load(GOLDEN / name)
     meta = json.loads(bytes(z["meta"]).decode())
     return [GoldenCase(m, z) for m in meta]
 
