@@ -10,7 +10,7 @@
 #include <string>
 #include <vector>
 
-#include "alert_kernels.cuh"
+#include "alert_baselines.cuh"
 
 using namespace alert;
 
@@ -151,6 +151,7 @@ __global__ void state_init_kernel(AlertState st, AlertFilterConfig cfg, double p
   st.m_var[i] = cfg.m0;
   st.group_budget[i] = 0.0;
   st.group_count[i] = 0;
+  if (st.policy_aux) st.policy_aux[i] = -1;  // comparison schemes: begin() pending
 }
 
 // Deterministic reduction: fixed chunks of streams per block, fixed order.
@@ -375,6 +376,19 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   size_t oA = place(sizeof(float4) * n), oB = place(sizeof(float4) * n), oC = place(sizeof(int2) * (cols.size() + 1));
   size_t oC64 = place(sizeof(Cell64) * n), oCell = place(4 * n);
   size_t oPw = place(8 * P);
+  size_t oSys = place(4 * P), oApp = place(4 * P);
+  // comparison-scheme cells (policies.py:283-454): per power, the sys-only
+  // DNN's cell and the first cell of the app-only DNN's column
+  std::vector<int> sys_cells(P, -1), app_first(P, -1);
+  int app_stages = 0;
+  if (d->sys_dnn >= 0 && d->sys_dnn < d->n_dnns && d->dnn_kind[d->sys_dnn] == ALERT_KIND_TRADITIONAL)
+    for (int c2 = 0; c2 < n; ++c2)
+      if (tb->cand_dnn[c2] == d->sys_dnn) sys_cells[tb->cand_power[c2]] = cell_of_cand[c2];
+  if (d->app_dnn >= 0 && d->app_dnn < d->n_dnns && d->dnn_kind[d->app_dnn] == ALERT_KIND_ANYTIME) {
+    app_stages = d->dnn_n_stages[d->app_dnn];
+    for (int c2 = 0; c2 < n; ++c2)
+      if (tb->cand_dnn[c2] == d->app_dnn && tb->cand_stage[c2] == 1) app_first[tb->cand_power[c2]] = cell_of_cand[c2];
+  }
   CUDA_TRY(cudaSetDevice(ctx->device));
   char* buf = nullptr;
   cudaError_t e = cudaMalloc(&buf, bytes);
@@ -389,6 +403,8 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   memcpy(&h[oC64], c64.data(), sizeof(Cell64) * n);
   memcpy(&h[oCell], cell_of_cand.data(), 4 * n);
   memcpy(&h[oPw], d->power_cap, 8 * P);
+  memcpy(&h[oSys], sys_cells.data(), 4 * P);
+  memcpy(&h[oApp], app_first.data(), 4 * P);
   e = cudaMemcpy(buf, h.data(), bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     cudaFree(buf);
@@ -408,6 +424,9 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   double r = d->p_idle_prof / max_cap;
   T.phi0 = (1.0 < r) ? 1.0 : r;  // min(1.0, p_idle_prof / max cap), policies.py:90
   T.power_cap64 = reinterpret_cast<const double*>(buf + oPw);
+  T.sys_cells = sys_cells[0] >= 0 ? reinterpret_cast<const int*>(buf + oSys) : nullptr;
+  T.app_first = app_stages > 0 ? reinterpret_cast<const int*>(buf + oApp) : nullptr;
+  T.app_stages = app_stages;
   T.cap_max = (float)max_cap;
   T.any_mono = 1;  // fast scan's anytime skip (fast_min_energy): stage latencies non-decreasing
   for (const int2& cd : cols)
@@ -612,6 +631,50 @@ int alert_state_init(AlertContext* ctx, const AlertTable* tb, const AlertFilterC
   return ALERT_OK;
 }
 
+// Comparison schemes (alert_baselines.cuh): oracle-static's begin() for the
+// streams whose policy_aux is still -1, then the one-thread-per-stream loop.
+static int run_baseline(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* cfg,
+                        const AlertSpec* specs, int n_specs, const int32_t* stream_spec, const AlertTrace* tr,
+                        AlertState st, const AlertOutputs* out, int policy, int64_t stream_begin,
+                        int64_t stream_end, int64_t step_begin, int64_t step_end, cudaStream_t s) {
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  SpecDev* dspecs = nullptr;
+  int r = upload_specs(specs, n_specs, tb, s, &dspecs);
+  if (r) return r;
+  BaseParams B;
+  B.T = tb->dev;
+  B.cfg = *cfg;
+  B.specs = dspecs;
+  B.n_specs = n_specs;
+  B.stream_spec = stream_spec;
+  B.tr = *tr;
+  B.st = st;
+  B.out = *out;
+  B.policy = policy;
+  B.stream_begin = stream_begin;
+  B.stream_end = stream_end;
+  B.step_begin = step_begin;
+  B.step_end = step_end;
+  const long long n = stream_end - stream_begin;
+  if (policy == ALERT_POLICY_ORACLE_STATIC) {
+    static_choice_kernel<<<(unsigned)n, 128, 0, s>>>(B);
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches++;
+  }
+  const unsigned grid = (unsigned)((n + 127) / 128);
+  switch (policy) {
+    case ALERT_POLICY_ORACLE_STATIC: baseline_kernel<ALERT_POLICY_ORACLE_STATIC><<<grid, 128, 0, s>>>(B); break;
+    case ALERT_POLICY_SYS_ONLY: baseline_kernel<ALERT_POLICY_SYS_ONLY><<<grid, 128, 0, s>>>(B); break;
+    case ALERT_POLICY_APP_ONLY: baseline_kernel<ALERT_POLICY_APP_ONLY><<<grid, 128, 0, s>>>(B); break;
+    default: baseline_kernel<ALERT_POLICY_NO_COORD><<<grid, 128, 0, s>>>(B); break;
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(dspecs, s);
+  if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("baseline_kernel: ") + cudaGetErrorString(e));
+  ctx->launches++;
+  return ALERT_OK;
+}
+
 int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* cfg, const AlertSpec* specs,
               int32_t n_specs, const int32_t* stream_spec, const AlertTrace* tr, AlertState st,
               const AlertOutputs* out, int32_t policy, uint32_t flags, int64_t stream_begin, int64_t stream_end,
@@ -619,9 +682,16 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   if (!ctx || !tb || !cfg || !tr || !out) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: NULL argument");
   int r = check_specs(specs, n_specs);
   if (r) return r;
-  if (policy < ALERT_POLICY_ALERT || policy > ALERT_POLICY_ALERT_WITH_ORACLE)
+  if (policy < ALERT_POLICY_ALERT || policy > ALERT_POLICY_NO_COORD)
     return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: unknown policy");
-  int kinds = kinds_of(policy, tb);
+  const bool baseline = policy >= ALERT_POLICY_ORACLE_STATIC;
+  if (policy == ALERT_POLICY_SYS_ONLY && !tb->dev.sys_cells)
+    return fail(ALERT_ERR_NO_CANDIDATE, "alert_run: sys-only needs a traditional DNN (AlertSpaceDesc.sys_dnn)");
+  if ((policy == ALERT_POLICY_APP_ONLY || policy == ALERT_POLICY_NO_COORD) && !tb->dev.app_first)
+    return fail(ALERT_ERR_NO_CANDIDATE, "alert_run: space has no anytime DNN (AlertSpaceDesc.app_dnn)");
+  if ((policy == ALERT_POLICY_ORACLE_STATIC || policy == ALERT_POLICY_NO_COORD) && !st.policy_aux)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: this policy needs AlertState.policy_aux");
+  int kinds = baseline ? 3 : kinds_of(policy, tb);
   if (!kinds) return fail(ALERT_ERR_NO_CANDIDATE, "alert_run: space has no DNN of the policy's kinds");
   if (!tr->slowdown || !tr->n_segments || !tr->seg_end || !tr->seg_phase || !tr->seg_idle || tr->max_segments < 1)
     return fail(ALERT_ERR_INVALID_TRACE, "alert_run: incomplete trace description");
@@ -643,6 +713,8 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
       (out->stream_stride == 0 && out->step_stride == 0))
     return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: per-step outputs need strides");
   if (stream_end == stream_begin || step_end == step_begin) return ALERT_OK;
+  if (baseline) return run_baseline(ctx, tb, cfg, specs, n_specs, stream_spec, tr, st, out, policy, stream_begin,
+                                    stream_end, step_begin, step_end, (cudaStream_t)cuda_stream);
   int W = pick_lanes(ctx, tb);
   RunParams P;
   auto stage = [&](int tpb) {

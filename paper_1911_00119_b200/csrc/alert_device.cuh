@@ -48,7 +48,12 @@ struct DevTable {
   const int* cell_of_cand;
   const double* power_cap64;  // [n_powers] caps by power index
   double phi0;            // min(1, p_idle_prof / max cap), policies.py:90
-  int any_mono;           // every anytime column's t_prof grows >= 1e-5 relative per stage
+  int any_mono;           // every anytime column's t_prof is non-decreasing per stage
+  // comparison schemes (alert_baselines.cuh): cells of the sys-only DNN per
+  // power, first cell of the app-only / no-coord DNN's column per power
+  const int* sys_cells;   // [n_powers] or null
+  const int* app_first;   // [n_powers] or null
+  int app_stages;
   float cap_max;          // largest cap (FP32 error bound of the oracle scan)
 };
 

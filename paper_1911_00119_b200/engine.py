@@ -17,7 +17,7 @@ from ._lib import check, load
 from .packing import PackedSpace, filter_config, pack_space
 
 STATE_DTYPES = {"mu": "f8", "sigma2": "f8", "k_gain": "f8", "q_noise": "f8", "innov": "f8", "phi": "f8",
-                "m_var": "f8", "group_budget": "f8", "group_count": "i4"}
+                "m_var": "f8", "group_budget": "f8", "group_count": "i4", "policy_aux": "i4"}
 
 
 def _torch():

@@ -23,9 +23,8 @@ from .model import DnnKind, kind_of
 from .packing import pack_specs
 from .records import decision_of
 
-POLICY_NAMES = ("alert", "alert-any", "alert-trad", "oracle")
-# Reference policies outside the accelerated hot path (SURVEY.md §8(f) "next").
-NEXT_POLICY_NAMES = ("oracle-static", "sys-only", "app-only", "no-coord")
+POLICY_NAMES = ("alert", "alert-any", "alert-trad", "oracle", "oracle-static", "sys-only", "app-only",
+                "no-coord")
 
 
 class GpuPolicy:
@@ -149,6 +148,39 @@ class OraclePolicy(GpuPolicy):
         pass
 
 
+class BaselinePolicy(GpuPolicy):
+    """The reference's comparison schemes (policies.py:211-454) on the GPU:
+    oracle-static (best fixed candidate over the realized trace), sys-only
+    (fastest traditional DNN, cheapest on-time power cap), app-only (one
+    anytime DNN at the maximum cap, best expected-accuracy stage), no-coord
+    (both controllers, uncoordinated).  They run through the fused path
+    (:func:`paper_1911_00119_b200.run` / ``run_batch``: one launch per
+    trace, FP64 with the reference's operation order)."""
+
+    def __init__(self, name: str, kalman: KalmanConfig | None = None, device: int = 0):
+        self.name = name
+        self.code_name = name
+        self.kalman = kalman
+        self.device = device
+
+    def begin(self, space, spec, env) -> None:
+        from .packing import baseline_dnns
+
+        sys_dnn, app_dnn = baseline_dnns(space)
+        if self.name == "sys-only" and sys_dnn < 0:
+            raise ValueError("no DNN of kind DnnKind.TRADITIONAL in the space")  # model.py:172-173
+        if self.name in ("app-only", "no-coord") and app_dnn < 0:
+            raise ValueError("space has no anytime DNN")  # policies.py:327-328
+        self.space, self.spec, self.env = space, spec, env
+
+    def decide(self, index: int, t_goal: float):
+        raise NotImplementedError(f"{self.name}: the comparison schemes run fused over a whole trace "
+                                  "(paper_1911_00119_b200.run / run_batch), not step by step")
+
+    def observe(self, record) -> None:
+        raise NotImplementedError(f"{self.name}: use paper_1911_00119_b200.run / run_batch")
+
+
 def make_policy(name: str, kalman: KalmanConfig | None = None, device: int = 0):
     """Registry with the reference's names (policies.py:469-490)."""
     if name == "alert":
@@ -160,6 +192,6 @@ def make_policy(name: str, kalman: KalmanConfig | None = None, device: int = 0):
                            device=device)
     if name == "oracle":
         return OraclePolicy(device=device)
-    if name in NEXT_POLICY_NAMES:
-        raise NotImplementedError(f"policy {name!r} is outside the accelerated hot path (SURVEY.md §8(f))")
+    if name in ("oracle-static", "sys-only", "app-only", "no-coord"):
+        return BaselinePolicy(name, kalman=kalman, device=device)
     raise ValueError(f"unknown policy {name!r}; choose from {POLICY_NAMES}")

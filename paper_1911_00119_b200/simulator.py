@@ -114,6 +114,8 @@ def run_batch(space, specs: Sequence, envs, policy: str = "alert", *, kalman=Non
     if out.step_stride == 0:
         out.step_stride, out.stream_stride = ns, 1
     chunk = chunk_steps or steps
+    if pol == abi.POLICY_ORACLE_STATIC:
+        chunk = steps  # begin() is clairvoyant over the whole trace (policies.py:221-265)
     for s0 in range(0, steps, chunk):
         eng.run(table, spec_arr, trace, state, policy=pol, kalman=kalman, idle_cfg=idle_cfg, stream_spec=ss,
                 outputs=out, flags=flags, stream_end=ns, step_begin=s0, step_end=min(steps, s0 + chunk))
@@ -147,6 +149,9 @@ class HostStreamer:
         self.specs = specs if isinstance(specs, np.ndarray) and specs.dtype == abi.SPEC_DTYPE \
             else pack_specs(list(specs), group_sizes)
         self.policy = policy_code(policy)
+        if self.policy == abi.POLICY_ORACLE_STATIC:
+            raise ValueError("oracle-static is clairvoyant over the whole trace: use run_batch (device-resident "
+                             "trace), not the chunked host streamer")
         self.kalman, self.idle_cfg = kalman, idle_cfg
         self.n_steps, self.n_streams = packed.slowdown.shape
         self.chunk = min(chunk_steps, self.n_steps)

@@ -82,5 +82,21 @@ def test_make_policy_names():
         assert A.make_policy(n).name == n
     with pytest.raises(ValueError, match="unknown policy"):
         A.make_policy("greedy")
-    with pytest.raises(NotImplementedError):
-        A.make_policy("sys-only")
+    assert set(A.POLICY_NAMES) == {"alert", "alert-any", "alert-trad", "oracle", "oracle-static", "sys-only",
+                                   "app-only", "no-coord"}  # policies.py:457-466
+
+
+def test_baseline_dnn_choice_matches_reference_rules():
+    """sys-only: fastest final-stage latency at the last power, ties to the
+    lower id (model.py:166-176); app-only: most stages, ties to the higher id
+    (policies.py:324-329)."""
+    from paper_1911_00119_b200.packing import baseline_dnns, pack_space
+
+    space = A.preset_space()
+    assert baseline_dnns(space) == (0, 7)  # dnn-00 is the fastest traditional DNN; any-07 the anytime one
+    d = pack_space(space).desc
+    assert (d.sys_dnn, d.app_dnn) == (0, 7)
+    only_any = A.ConfigSpace(tuple(x for x in space.dnns if x.id == "any-07"), space.powers, space.p_idle_prof)
+    assert baseline_dnns(only_any) == (-1, 0)
+    with pytest.raises(ValueError, match="TRADITIONAL"):
+        A.make_policy("sys-only").begin(only_any, None, None)
