@@ -5,7 +5,9 @@ Run in the build container, where /root/reference exists:
 Writes tests/golden/golden_runs.npz and tests/golden/golden_predict.npz;
     python tests/golden/make_golden.py --baselines
 writes tests/golden/golden_baselines.npz (the comparison schemes
-oracle-static / sys-only / app-only / no-coord).
+oracle-static / sys-only / app-only / no-coord, SURVEY.md §8(f));
+    python tests/golden/make_golden.py --sweeps
+writes tests/golden/golden_sweeps.json (cmd_sweep CSV output).
 The reference is imported read-only from /root/reference/pkg/src; nothing at
 test time reads /root/reference — only these committed fixtures.
 """
@@ -288,8 +290,45 @@ def baselines():
     np.savez_compressed(OUT / "golden_baselines.npz", **arrays)
 
 
+def sweeps():
+    """CSV output of the reference's cmd_sweep (cli.py:191-274) on the preset
+    profile / preset trace (phase_length 100), for the GPU sweep driver."""
+    import tempfile
+
+    from alertsim.cli import main as cli_main
+    from alertsim.model import save_profile
+    from alertsim.simulator import save_trace
+
+    pols = "alert,alert-any,alert-trad,oracle,oracle-static,sys-only,app-only,no-coord"
+    runs = [
+        dict(mode="min-energy", goals="0.7,0.85", pr_th=None, seed=None),
+        dict(mode="max-accuracy", goals="0.5,0.8", pr_th=0.95, seed=None),
+        dict(mode="min-energy", goals="0.68", pr_th=None, seed=7),
+    ]
+    out = []
+    with tempfile.TemporaryDirectory() as d:
+        prof, tr = Path(d) / "profile.json", Path(d) / "trace.json"
+        save_profile(preset_space(), prof)
+        save_trace(preset_trace(phase_length=100), tr)
+        for r in runs:
+            csv_path = Path(d) / "sweep.csv"
+            argv = ["sweep", "--profile", str(prof), "--trace", str(tr), "--mode", r["mode"],
+                    "--q-goals" if r["mode"] == "min-energy" else "--e-goal-mults", r["goals"],
+                    "--policies", pols, "--out", str(csv_path)]
+            if r["pr_th"] is not None:
+                argv += ["--pr-th", str(r["pr_th"])]
+            if r["seed"] is not None:
+                argv += ["--seed", str(r["seed"])]
+            assert cli_main(argv) == 0
+            out.append(dict(r, policies=pols, phase_length=100, csv=csv_path.read_text()))
+            print(r, len(out[-1]["csv"].splitlines()), "rows")
+    (OUT / "golden_sweeps.json").write_text(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
-    if "--baselines" in sys.argv:
+    if "--sweeps" in sys.argv:
+        sweeps()
+    elif "--baselines" in sys.argv:
         baselines()
     else:
         main()
