@@ -377,6 +377,25 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   size_t oC64 = place(sizeof(Cell64) * n), oCell = place(4 * n);
   size_t oPw = place(8 * P);
   size_t oSys = place(4 * P), oApp = place(4 * P);
+  // max-accuracy fast scan units: traditional cells and anytime columns,
+  // sorted by accuracy upper bound (max of q_fail and the stage accuracies)
+  struct Unit { int first, n; double bound; };
+  std::vector<Unit> units;
+  for (int cell = 0; cell < (int)trad_cells.size(); ++cell)
+    units.push_back({cell, 1, std::max(c64[cell].a, c64[cell].qf)});
+  for (const int2& cd : cols) {
+    double b = c64[cd.x].qf;
+    for (int k = 0; k < cd.y; ++k) b = std::max(b, c64[cd.x + k].a);
+    units.push_back({cd.x, cd.y | (1 << 16), b});
+  }
+  std::stable_sort(units.begin(), units.end(), [](const Unit& a, const Unit& b) { return a.bound > b.bound; });
+  std::vector<int2> unit_v(units.size());
+  std::vector<float> unit_lb(units.size());
+  for (size_t k = 0; k < units.size(); ++k) {
+    unit_v[k] = make_int2(units[k].first, units[k].n);
+    unit_lb[k] = (float)(2.0 - units[k].bound) - 1e-5f;
+  }
+  size_t oUnit = place(sizeof(int2) * units.size()), oUlb = place(4 * units.size());
   // comparison-scheme cells (policies.py:283-454): per power, the sys-only
   // DNN's cell and the first cell of the app-only DNN's column
   std::vector<int> sys_cells(P, -1), app_first(P, -1);
@@ -404,6 +423,10 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   memcpy(&h[oCell], cell_of_cand.data(), 4 * n);
   memcpy(&h[oPw], d->power_cap, 8 * P);
   memcpy(&h[oSys], sys_cells.data(), 4 * P);
+  if (!units.empty()) {
+    memcpy(&h[oUnit], unit_v.data(), sizeof(int2) * units.size());
+    memcpy(&h[oUlb], unit_lb.data(), 4 * units.size());
+  }
   memcpy(&h[oApp], app_first.data(), 4 * P);
   e = cudaMemcpy(buf, h.data(), bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -425,6 +448,9 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   T.phi0 = (1.0 < r) ? 1.0 : r;  // min(1.0, p_idle_prof / max cap), policies.py:90
   T.power_cap64 = reinterpret_cast<const double*>(buf + oPw);
   T.sys_cells = sys_cells[0] >= 0 ? reinterpret_cast<const int*>(buf + oSys) : nullptr;
+  T.units = units.empty() ? nullptr : reinterpret_cast<const int2*>(buf + oUnit);
+  T.unit_lb = units.empty() ? nullptr : reinterpret_cast<const float*>(buf + oUlb);
+  T.n_units = (int)units.size();
   T.app_first = app_stages > 0 ? reinterpret_cast<const int*>(buf + oApp) : nullptr;
   T.app_stages = app_stages;
   T.cap_max = (float)max_cap;
@@ -509,10 +535,15 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
   P.fast_smem = 0;
   // row mode for large tables (no staged per-cell rows / per-tile thresholds)
   P.fast_rows = T.n_trad > 512 || (flags & ALERT_FLAG_FAST_ROWS);
-  if (any_min_energy && policy != ALERT_POLICY_ORACLE && !(flags & (ALERT_FLAG_NO_FAST | ALERT_FLAG_FP64_ALL)) &&
+  P.units_smem = 0;
+  const bool any_max_accuracy = !all_min_energy;
+  if ((any_min_energy || any_max_accuracy) && policy != ALERT_POLICY_ORACLE &&
+      !(flags & (ALERT_FLAG_NO_FAST | ALERT_FLAG_FP64_ALL)) &&
       ALERT_MAX_STAGES <= 8 &&
       (P.fast_rows || (size_t)(tpb / W) * (size_t)(n_tdnn + 1) * 2 * sizeof(float) <= 16 * 1024))
     P.fast_smem = 1;  // alert_run computes the thresholds (zlo_kernel) and sets P.zlo
+  // max-accuracy fast scan needs its sorted units in shared memory
+  if (P.fast_smem && any_max_accuracy && T.units && T.n_units <= 1024) P.units_smem = 1;
   P.c64_smem = T.n_cells <= kC64SmemMax;
   P.ratio_smem = T.n_powers <= kRatioSmemMax &&
                  (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;
@@ -529,7 +560,8 @@ static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const 
   SmemLayout L(T.n_cells, T.n_any_cols, tpb / W, P.c64_smem ? T.n_cells : 0, tpb / W,
                P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
                (P.fast_smem && !P.fast_rows) ? T.n_trad / T.n_powers : 0,
-               (P.fast_smem && !P.fast_rows) ? T.n_trad : 0, P.fast_smem && !P.fast_rows);
+               (P.fast_smem && !P.fast_rows) ? T.n_trad : 0, P.fast_smem && !P.fast_rows,
+               P.units_smem ? T.n_units : 0);
   return L.total;
 }
 

@@ -51,6 +51,11 @@ struct DevTable {
   int any_mono;           // every anytime column's t_prof is non-decreasing per stage
   // comparison schemes (alert_baselines.cuh): cells of the sys-only DNN per
   // power, first cell of the app-only / no-coord DNN's column per power
+  // max-accuracy fast scan (fast_max_accuracy): units = traditional cells and
+  // anytime columns sorted by their accuracy upper bound, descending
+  const int2* units;      // {first cell, n cells | anytime << 16}
+  const float* unit_lb;   // lower bound of any key of the unit: 2 - bound - 1e-5
+  int n_units;
   const int* sys_cells;   // [n_powers] or null
   const int* app_first;   // [n_powers] or null
   int app_stages;
@@ -170,6 +175,8 @@ struct StepCtx {
   const float4* sF;  // traditional cells {1/t, cap t, byte offset of the DNN's threshold in tT, 0}
   const float* zrow; // row mode (large tables): the spec's z' per traditional DNN (global, L1)
   const unsigned* wst;  // per 32-cell window of anytime cells: column-start bits (shared)
+  const int2* su;       // max-accuracy fast scan: units / key lower bounds staged in shared memory
+  const float* slb;
   float hs, hm;      // T_d = fma(z'_d, hs, hm)
   float Tpr;     // same for the pr_threshold z-bound (anytime cells)
 };
@@ -194,6 +201,8 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
   x.sF = nullptr;
   x.zrow = nullptr;
   x.wst = nullptr;
+  x.su = nullptr;
+  x.slb = nullptr;
   x.hs = x.hm = 0.f;
   x.Tpr = -kInfF;
   x.mu = mu;
@@ -827,6 +836,191 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
   return true;
 }
 
+// --------------------------------------------------------------------------
+// Max-accuracy fast scan (level 0 of selector.py:102-131 in MAXIMIZE_ACCURACY:
+// Pr >= pr_th and E <= e_goal, objective (-acc, E, power, dnn, stage)).
+//
+// Units (traditional cells and anytime columns) are visited in descending
+// order of their accuracy upper bound (max of q_fail and the stage
+// accuracies: expected accuracy is a convex combination of them); keys are
+// 2 - acc with the L0 constraints folded in as sign-exact penalties (pr via
+// the z-bound T_pr, energy via E - e_lo), so the warp stops as soon as no
+// remaining unit can reach the current second-best key P2.
+//
+// Certified when P1's cell is surely feasible and either
+//  (b) P2 exceeds P1 by more than the FP32 accuracy error, or
+//  (c) every key within that margin belongs to a cell whose deadline
+//      probability is EXACTLY 1 in FP64 (z >= 8.6: erfc below 2^-53, so
+//      0.5 (1 + erf) rounds to 1 and the expected accuracy equals the stage
+//      accuracy bit for bit) of P1's accuracy class: the reference then ranks
+//      them by energy, resolved here in FP32 unless the energies are within
+//      their error bound.
+// Otherwise the full scan runs.
+constexpr float kExactOneX = 6.0811183f;  // z = 8.6 in units of z / sqrt 2
+
+template <bool HAS_PR, class Tile>
+__device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float4* __restrict__ sA,
+                                                  const float4* __restrict__ sB, const Tile& tile,
+                                                  const StepCtx& x, int kinds, Decision& d) {
+  const int W = Tile::num_threads();
+  const int lane = tile.thread_rank();
+  const float mgH = -x.goal_f * kPenH;
+  const float elH = -x.e_lo * kPenH;
+  const int n_units = T.n_units;
+  const int2* __restrict__ sU = x.su;      // units staged in shared memory
+  const float* __restrict__ sLb = x.slb;
+  // key of one cell, its energy and exact-one flag (running accuracy carried)
+  auto cell_key = [&](const float4& A, float& acc, bool& one, unsigned k, float& E) {
+    const float xz = fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s;
+    acc = fmaf(phi32_x(xz), A.z, acc);
+    one = one && xz >= kExactOneX;
+    E = A.y * fmaxf(x.mu_e, fmaf(x.phig, A.x, x.ompmu));
+    float pen = fmaf(E, kPenH, elH);
+    if (HAS_PR) pen = fmaxf(pen, fmaf(mgH, A.x, x.Tpr));
+    return pack_key(fmaxf(2.0f - acc, pen), k);
+  };
+  Top2 t{kInfF, kInfF, -1};
+  // pass 1: units in bound order; a lane stops at its first unit whose key
+  // lower bound reaches its running P2 (sorted: no later unit can matter)
+  for (int u = lane; u < n_units; u += W) {
+    if (sLb[u] >= t.p2) break;
+    const int2 un = sU[u];
+    if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
+    const int n = un.y & 0xFFFF;
+    float acc = sA[un.x].w;
+    bool one = true;
+    for (int k = 0; k < n; ++k) {
+      float E;
+      const float before = t.p1;
+      t.push(cell_key(sA[un.x + k], acc, one, (unsigned)k, E));
+      if (t.p1 != before) t.blk = un.x;
+    }
+  }
+  t.merge(tile);
+  if (!(t.p1 < 2.0f) || t.blk < 0) return false;  // P1 must be a possible cell (no penalty)
+  const int c1 = t.blk + (int)(__float_as_uint(t.p1) & 7u);
+  if (c1 >= T.n_cells) return false;
+  // sureness of a cell at level 0: energy and deadline probability
+  auto sure = [&](int c) {
+    const float4 A = sA[c];
+    const float E = A.y * fmaxf(x.mu_e, fmaf(x.phig, A.x, x.ompmu));
+    if (!(E <= x.e_hi)) return false;
+    if (!HAS_PR) return true;
+    return phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s) >= x.th_hi;
+  };
+  const float cut = t.p1 + 2.0f * x.d_acc + 4e-6f;  // + truncation of both keys
+  if (t.p2 > cut) {  // (b) strict accuracy winner (keys distinct: blk is P1's unit)
+    if (!sure(c1)) return false;
+    d.cell = c1;
+    d.level = 0;
+    d.refined = false;
+    return true;
+  }
+  if (W == 1) {
+    // (c') one lane per stream: near-ties within P1's class (same DNN and
+    // target stage) are ordered by the deadline-miss tail T = sum_m h_m d_m
+    // (acc = a_k - T exactly; h_m = erfc(x_m) / 2, relatively accurate via
+    // erfcf, 0 when x_m >= kExactOneX where FP64 rounds Pr to exactly 1):
+    // the smaller tail wins unless the intervals T (1 -+ r) (r from the FP32
+    // error of x_m) come within 2.5e-15 (FP64 blend rounding and the 2^-53
+    // quantisation of Pr); equal zero tails tie exactly and go by energy.
+    const uint32_t ccls = __float_as_uint(sB[c1].y) & 0xFFFFFu;  // dnn << 8 | stage
+    bool ok1 = true;
+    float ze1 = kInfF, ze2 = kInfF, bh = kInfF, bl = kInfF, lo2 = kInfF, nzlo = kInfF;
+    int zc = -1, bc = -1;
+    for (int u = 0; u < n_units; ++u) {
+      if (sLb[u] > cut) break;
+      const int2 un = sU[u];
+      if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
+      const int n = un.y & 0xFFFF;
+      float acc = sA[un.x].w, tail = 0.f, r = 0.f;
+      bool one = true, bad = false;
+      for (int k = 0; k < n; ++k) {
+        const float4 A = sA[un.x + k];
+        float E;
+        const float xz = fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s;
+        const float key = cell_key(A, acc, one, (unsigned)k, E);
+        if (!(xz >= kExactOneX)) {
+          bad |= !(xz >= 0.0f) || !(A.z >= 0.0f);
+          tail = fmaf(0.5f * erfcf(xz), A.z, tail);
+          const float dx = 4.0f * kEps * (fmaf(x.goal_f, A.x, fabsf(x.mu_f)) * x.inv_sig_s + fabsf(xz));
+          r = fmaxf(r, fmaf(2.0f * xz + 2.0f, dx, 1e-5f));
+        }
+        if (key > cut) continue;
+        const int c = un.x + k;
+        if (bad || (__float_as_uint(sB[c].y) & 0xFFFFFu) != ccls) ok1 = false;
+        if (tail == 0.0f) {  // exact acc = a_k: energy decides among these
+          ze2 = fminf(ze2, fmaxf(ze1, E));
+          if (E < ze1) zc = c;
+          ze1 = fminf(ze1, E);
+        } else {
+          const float hi = tail * (1.0f + r), lo = tail * (1.0f - r);
+          nzlo = fminf(nzlo, lo);
+          if (hi < bh) {
+            lo2 = fminf(lo2, bl);
+            bh = hi; bl = lo; bc = c;
+          } else {
+            lo2 = fminf(lo2, lo);
+          }
+        }
+      }
+    }
+    int w;
+    if (!ok1) return false;
+    if (zc >= 0) {  // zero tails win; nonzero ones must be strictly worse
+      if (!(nzlo > 2.5e-15f) || !(ze2 > ze1 + ze1 * (4.0f * x.d_erel) + 1e-30f)) return false;
+      w = zc;
+    } else {
+      if (bc < 0 || !(lo2 > bh + 2.5e-15f)) return false;
+      w = bc;
+    }
+    if (!sure(w)) return false;
+    d.cell = w;
+    d.level = 0;
+    d.refined = false;
+    return true;
+  }
+  // (c) near-tie: every key <= cut must be an exact-one cell of P1's class;
+  // the winner is then the lowest energy among them (re-scan of the few
+  // units that can reach the cut)
+  const int cls = cell_rank_a(sB[c1]);
+  int ok = 1;
+  float e1 = kInfF, e2 = kInfF;
+  int ce = -1;
+  for (int u = lane; u < n_units; u += W) {
+    if (sLb[u] > cut) break;
+    const int2 un = sU[u];
+    if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
+    const int n = un.y & 0xFFFF;
+    float acc = sA[un.x].w;
+    bool one = true;
+    for (int k = 0; k < n; ++k) {
+      float E;
+      const float key = cell_key(sA[un.x + k], acc, one, (unsigned)k, E);
+      if (key > cut) continue;
+      if (!one || cell_rank_a(sB[un.x + k]) != cls) ok = 0;
+      e2 = fminf(e2, fmaxf(e1, E));
+      if (E < e1) ce = un.x + k;
+      e1 = fminf(e1, E);
+    }
+  }
+  // tile-wide: all lanes ok, the lowest energy and its runner-up
+#pragma unroll
+  for (int m = 1; m < W; m <<= 1) {
+    const float o1 = tile.shfl_xor(e1, m), o2 = tile.shfl_xor(e2, m);
+    const int oc = tile.shfl_xor(ce, m);
+    ok &= tile.shfl_xor(ok, m);
+    e2 = fmin3(e2, o2, fmaxf(e1, o1));
+    if (o1 < e1 || (o1 == e1 && oc >= 0 && (ce < 0 || oc < ce))) ce = oc;
+    e1 = fminf(e1, o1);
+  }
+  if (!ok || ce < 0 || ce >= T.n_cells || !(e2 > e1 + e1 * (4.0f * x.d_erel) + 1e-30f) || !sure(ce)) return false;
+  d.cell = ce;
+  d.level = 0;
+  d.refined = false;
+  return true;
+}
+
 // Re-rank pass from the stored FP32 objectives (no re-scan): the same
 // cell-to-lane assignment as cell_pass, so each lane reads what it wrote.
 template <int MODE, bool HAS_PR, class Tile>
@@ -957,9 +1151,22 @@ __device__ __forceinline__ Decision alert_decide_t(const DevTable& T, const floa
                                                    const int2* sCol, const Tile& tile, StepCtx& x, int kinds,
                                                    bool no_refine) {
   bool tried = false;
+  // the fast scans vote across the converged lanes (__activemask); the
+  // explicit __syncwarp re-converges them before the (divergent) fallback
   if (MODE == ALERT_MODE_MIN_ENERGY && x.fast && !x.fp64_all) {
+    const unsigned am = __activemask();
     Decision d{-1, 0, false};
-    if (fast_min_energy<HAS_PR>(T, sA, sB, sCol, tile, x, kinds, d)) return d;
+    const bool ok = fast_min_energy<HAS_PR>(T, sA, sB, sCol, tile, x, kinds, d);
+    __syncwarp(am);
+    if (ok) return d;
+    tried = true;
+  }
+  if (MODE == ALERT_MODE_MAX_ACCURACY && x.fast && !x.fp64_all && x.su) {
+    const unsigned am = __activemask();
+    Decision d{-1, 0, false};
+    const bool ok = fast_max_accuracy<HAS_PR>(T, sA, sB, tile, x, kinds, d);
+    __syncwarp(am);
+    if (ok) return d;
     tried = true;
   }
   Decision d = OUTLINE ? alert_decide_full_call<MODE, HAS_PR>(T, sA, sB, sCol, tile, x, kinds, no_refine)

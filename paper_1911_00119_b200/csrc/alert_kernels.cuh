@@ -32,6 +32,7 @@ struct RunParams {
   const float* zlo;
   int fast_smem;  // host: shared-memory slots for the fast scan staged
   int fast_rows;  // fast scan in row mode (large tables): no staged rows / thresholds
+  int units_smem; // max-accuracy fast scan: bound-sorted units staged in shared memory
   long long stream_begin, stream_end, step_begin, step_end;
   // Idle-filter gains (estimator.py:123-125) do not depend on the data: the
   // sequence M_k (state after k updates from m0) and W_k reaches an exact FP64
@@ -52,14 +53,14 @@ struct ColdState {
 
 // Shared-memory layout of run_kernel (host and device compute it identically).
 struct SmemLayout {
-  size_t B, col, spec, c64, ratio, agg, sv, fz, ff, wst, cold, slot, total;
+  size_t B, col, spec, c64, ratio, agg, sv, fz, ff, wst, un, cold, slot, total;
   __host__ __device__ static size_t up16(size_t x) { return (x + 15) & ~size_t(15); }
   // pad = look-ahead rows past the end of the cell / column tables for a tile
   // width W: 2 chunks of 4 cells (see cell_pass), so 8 W + 8.
   __host__ __device__ static int pad_rows(int W) { return 8 * W + 8; }
   __host__ __device__ SmemLayout(int n_cells, int n_cols, int n_spec, int n_c64, int n_tiles, int n_ratio,
                                  size_t agg_bytes, int n_sv, int W, int n_fz = 0, int n_ff = 0,
-                                 bool flat = false) {
+                                 bool flat = false, int n_un = 0) {
     B = sizeof(float4) * (size_t)(n_cells + pad_rows(W));
     col = B + sizeof(float4) * (size_t)n_cells;
     spec = up16(col + sizeof(int2) * (size_t)(n_cols + pad_rows(W)));
@@ -70,7 +71,8 @@ struct SmemLayout {
     fz = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);  // 2 x [n_fz][n_tiles]: Z, T
     ff = up16(fz + 2 * sizeof(float) * (size_t)n_tiles * (size_t)n_fz);  // fast-scan traditional cells
     wst = up16(ff + (flat ? sizeof(float4) * (size_t)(n_ff + pad_rows(W)) : 0));
-    cold = up16(wst + (flat ? sizeof(unsigned) * (size_t)(n_cells / 32 + 2) : 0));
+    un = up16(wst + (flat ? sizeof(unsigned) * (size_t)(n_cells / 32 + 2) : 0));  // units, then lbs
+    cold = up16(un + (sizeof(int2) + sizeof(float)) * (size_t)n_un);
     slot = up16(cold + sizeof(ColdState) * (size_t)n_tiles * (size_t)W);
     total = up16(slot + 16 * (size_t)n_tiles * (size_t)W);  // two 8-byte trace slots per thread
   }
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   const SmemLayout L(T.n_cells, T.n_any_cols, n_tiles, P.c64_smem ? T.n_cells : 0, n_tiles,
                      P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
                      (P.zlo && !P.fast_rows) ? n_tdnn : 0, (P.zlo && !P.fast_rows) ? T.n_trad : 0,
-                     P.zlo && !P.fast_rows);
+                     P.zlo && !P.fast_rows, P.units_smem ? T.n_units : 0);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
   float4* sB = reinterpret_cast<float4*>(base + L.B);
@@ -193,6 +195,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       const int off = in ? (i / T.n_powers) * n_tiles * (int)sizeof(float) : 0;
       sF[i] = make_float4(in ? T.cellA[i].x : 0.f, in ? T.cellA[i].y : 0.f, __int_as_float(off),
                           __int_as_float((i / W) & 7));
+    }
+  int2* sUn = reinterpret_cast<int2*>(base + L.un);
+  float* sLb = reinterpret_cast<float*>(sUn + (P.units_smem ? T.n_units : 0));
+  if (P.units_smem)
+    for (int i = threadIdx.x; i < T.n_units; i += blockDim.x) {
+      sUn[i] = T.units[i];
+      sLb[i] = T.unit_lb[i];
     }
   unsigned* sWst = reinterpret_cast<unsigned*>(base + L.wst);
   if (P.zlo && !P.fast_rows)  // column-start bits of the anytime cells, per 32-cell window
@@ -232,12 +241,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   const long long row = tr.stream_row ? tr.stream_row[stream] : stream_ll;
   // min-energy fast scan: the stream's z-thresholds, copied once into the
   // tile's interleaved shared slots (element d at [d * n_tiles + tile])
-  const bool fast = P.zlo && spec->mode == ALERT_MODE_MIN_ENERGY;
+  const bool fast = P.zlo && (spec->mode == ALERT_MODE_MIN_ENERGY || T.units);
+  const bool fast_me = fast && spec->mode == ALERT_MODE_MIN_ENERGY;  // per-DNN thresholds needed
   float zpr = -kInfF;
   if (fast) {
     const float* zrow = P.zlo + (size_t)si * (n_tdnn + 1);
     zpr = zrow[n_tdnn];
-    if (!P.fast_rows) {
+    if (!P.fast_rows && fast_me) {
       float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
       for (int d = tile.thread_rank(); d < n_tdnn; d += W) fzZ[d * n_tiles] = zrow[d];
       if (W > 1) tile.sync();
@@ -350,8 +360,12 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
         x.fast = true;
         x.sF = sF;
         x.wst = sWst;
+        if (P.units_smem) {
+          x.su = sUn;
+          x.slb = sLb;
+        }
         float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
-        fast_prep(x, tile, fzZ, fzZ + (size_t)n_tiles * n_tdnn, n_tiles, n_tdnn, zpr,
+        fast_prep(x, tile, fzZ, fzZ + (size_t)n_tiles * n_tdnn, n_tiles, fast_me ? n_tdnn : 0, zpr,
                   P.fast_rows ? P.zlo + (size_t)si * (n_tdnn + 1) : nullptr);
       }
       d = alert_decide<MS>(T, sA, sB, sCol, tile, x, P.kinds, P.flags & ALERT_FLAG_NO_REFINE);

@@ -225,9 +225,14 @@ def test_lane_widths_identical(lanes):
     base = A.run_batch(space, specs, envs, "alert", records="f64", trace_dtype=np.float64, lanes_per_stream=1)
     got = A.run_batch(space, specs, envs, "alert", records="f64", trace_dtype=np.float64, lanes_per_stream=lanes)
     A.get_engine().set_launch(0, 0)
-    np.testing.assert_array_equal(got.records["decision"], base.records["decision"])
+    # bit 26 / AGG_REFINED / AGG_FULL_SCAN record WHICH path decided (fast-scan
+    # certification differs by width: one-lane tail ordering); the decisions may not
+    path_bits = ~np.int32(1 << 26)
+    np.testing.assert_array_equal(got.records["decision"] & path_bits, base.records["decision"] & path_bits)
     np.testing.assert_array_equal(got.records["energy"], base.records["energy"])
-    np.testing.assert_array_equal(got.agg, base.agg)
+    keep = np.ones(abi.AGG_FIELDS, bool)
+    keep[[abi.AGG_REFINED, abi.AGG_FULL_SCAN]] = False
+    np.testing.assert_array_equal(got.agg[:, keep], base.agg[:, keep])
 
 
 def test_fp64_all_equals_fast_path():
@@ -280,6 +285,47 @@ def test_fast_scan_equals_full_scan(seed):
     np.testing.assert_array_equal(fast.records["energy"], full.records["energy"])
     np.testing.assert_array_equal(fast.agg[:, :abi.AGG_LEVEL0], full.agg[:, :abi.AGG_LEVEL0])
     for k in range(0, len(envs), 5):
+        rec, _, _ = oracle.run(space, specs[k % len(specs)], envs[k], policy)
+        own = A.run_batch(space, [specs[k % len(specs)]], [envs[k]], policy, records="f64",
+                          trace_dtype=np.float64, forced=rec["cand"][:, None].astype(np.int32))
+        assert_decisions(own.decoded()["cand"][:, 0], rec, f"seed {seed} stream {k}")
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fast_max_accuracy_equals_full_scan(seed):
+    """The max-accuracy fast scan (bound-sorted units, certified top-2,
+    exact-one accuracy ties resolved by energy) changes no decision or value
+    against the full scan; constant-slow-down phases drive sigma down so that
+    many deadline probabilities are exactly 1 (the tie case)."""
+    rnd = random.Random(9090 + seed)
+    space = random_space(rnd, 6, 6) if seed % 2 else A.preset_space()
+    specs = []
+    ref = A.reference_latency(space)
+    for k in range(6):
+        t = ref * rnd.uniform(0.4, 2.0)
+        pr = [None, 0.95, rnd.uniform(0.05, 0.99)][k % 3]
+        specs.append(A.ConstraintSpec(mode=A.Mode.MAXIMIZE_ACCURACY, t_goal=t,
+                                      e_goal=rnd.uniform(0.2, 1.0) * space.max_power.cap_watts * t,
+                                      pr_threshold=pr, overhead_budget=0.01 * ref))
+    envs = []
+    for k in range(30):
+        phases = (A.EnvironmentPhase(80, A.Constant(rnd.uniform(0.5, 1.5)), rnd.uniform(1, 9), 0.0),
+                  A.EnvironmentPhase(60, A.LogNormal(rnd.uniform(-0.2, 0.7), 0.3), rnd.uniform(1, 9), 0.05),
+                  A.EnvironmentPhase(60, A.Constant(rnd.uniform(0.8, 2.0)), rnd.uniform(1, 9), 0.01))
+        envs.append(A.realize(A.Trace(seed=rnd.randint(0, 2**31), phases=phases)))
+    policy = ["alert", "alert-any", "alert-trad"][seed % 3]
+    lanes = [1, 2, 4, 8][seed % 4]
+    try:
+        fast = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64, lanes_per_stream=lanes)
+    except Exception:
+        pytest.skip("space has no DNN of the policy's kinds")
+    full = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64, lanes_per_stream=lanes,
+                       flags=abi.FLAG_NO_FAST)
+    A.get_engine().set_launch(0, 0)
+    np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
+    np.testing.assert_array_equal(fast.records["energy"], full.records["energy"])
+    np.testing.assert_array_equal(fast.agg[:, :abi.AGG_LEVEL0], full.agg[:, :abi.AGG_LEVEL0])
+    for k in range(0, len(envs), 7):
         rec, _, _ = oracle.run(space, specs[k % len(specs)], envs[k], policy)
         own = A.run_batch(space, [specs[k % len(specs)]], [envs[k]], policy, records="f64",
                           trace_dtype=np.float64, forced=rec["cand"][:, None].astype(np.int32))
