@@ -881,18 +881,44 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
   };
   Top2 t{kInfF, kInfF, -1};
   // pass 1: units in bound order; a lane stops at its first unit whose key
-  // lower bound reaches its running P2 (sorted: no later unit can matter)
+  // lower bound reaches its running P2 (sorted: no later unit can matter).
+  // With the per-tile store (x.has_sv) every key is kept for the near-tie
+  // pass, which then re-derives only the tails of the few tied cells.
+  const bool store = W == 1 && x.has_sv;
+  int u_end = lane;
   for (int u = lane; u < n_units; u += W) {
     if (sLb[u] >= t.p2) break;
+    u_end = u + W;
     const int2 un = sU[u];
     if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
     const int n = un.y & 0xFFFF;
     float acc = sA[un.x].w;
     bool one = true;
     for (int k = 0; k < n; ++k) {
+      const float4 A = sA[un.x + k];
+      // constraints first (no Phi): a cell that is surely infeasible at L0
+      // cannot enter (P1, P2); with non-decreasing stage latencies every
+      // later stage of the column is infeasible too (Pr falls, E grows —
+      // the energy test then uses a 2 d_erel margin to absorb FP64 rounding)
+      const float E0 = A.y * fmaxf(x.mu_e, fmaf(x.phig, A.x, x.ompmu));
+      const float pp = HAS_PR ? fmaf(mgH, A.x, x.Tpr) : -kInfF;
+      if (fmaxf(fmaf(E0, kPenH, elH), pp) > 0.0f) {
+        if (store) asm volatile("st.shared.f32 [%0], %1;" ::"r"(x.sv + 4u * (un.x + k)), "f"(kInfF));
+        const bool later_out = pp > 0.0f || E0 > x.e_lo * (1.0f + x.d_erel);
+        if (T.any_mono && later_out) {
+          for (int k2 = k + 1; k2 < n && store; ++k2)
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(x.sv + 4u * (un.x + k2)), "f"(kInfF));
+          break;
+        }
+        acc = fmaf(phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s), A.z, acc);  // carry only
+        one = false;
+        continue;
+      }
       float E;
       const float before = t.p1;
-      t.push(cell_key(sA[un.x + k], acc, one, (unsigned)k, E));
+      const float key = cell_key(A, acc, one, (unsigned)k, E);
+      if (store) asm volatile("st.shared.f32 [%0], %1;" ::"r"(x.sv + 4u * (un.x + k)), "f"(key));
+      t.push(key);
       if (t.p1 != before) t.blk = un.x;
     }
   }
@@ -933,6 +959,15 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
       const int2 un = sU[u];
       if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
       const int n = un.y & 0xFFFF;
+      if (store && u < u_end) {  // keys kept by pass 1: skip units with no key <= cut
+        bool any = false;
+        for (int k = 0; k < n; ++k) {
+          float kk;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(kk) : "r"(x.sv + 4u * (un.x + k)));
+          any |= kk <= cut;
+        }
+        if (!any) continue;
+      }
       float acc = sA[un.x].w, tail = 0.f, r = 0.f;
       bool one = true, bad = false;
       for (int k = 0; k < n; ++k) {
