@@ -29,7 +29,10 @@ STALLS = "smsp__average_warps_issue_stalled_"
 
 
 def summarize(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # raw page exported on the GPU box
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, vals = rows[0], rows[2:]
     res = []
