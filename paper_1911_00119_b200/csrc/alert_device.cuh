@@ -958,15 +958,16 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
       if (sLb[u] > cut) break;
       const int2 un = sU[u];
       if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
-      const int n = un.y & 0xFFFF;
-      if (store && u < u_end) {  // keys kept by pass 1: skip units with no key <= cut
-        bool any = false;
+      int n = un.y & 0xFFFF;
+      if (store && u < u_end) {  // keys kept by pass 1: the chain only up to the last key <= cut
+        int last = -1;
         for (int k = 0; k < n; ++k) {
           float kk;
           asm volatile("ld.shared.f32 %0, [%1];" : "=f"(kk) : "r"(x.sv + 4u * (un.x + k)));
-          any |= kk <= cut;
+          if (kk <= cut) last = k;
         }
-        if (!any) continue;
+        if (last < 0) continue;
+        n = last + 1;
       }
       float acc = sA[un.x].w, tail = 0.f, r = 0.f;
       bool one = true, bad = false;
