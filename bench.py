@@ -55,7 +55,7 @@ def log(*a):
 # --------------------------------------------------------------------------
 # workloads
 
-def build_workload(cfg: str, n_streams: int, n_steps: int, rank: int):
+def build_workload(cfg: str, n_streams: int, n_steps: int, rank: int, world: int = 1):
     import paper_1911_00119_b200 as A
     from paper_1911_00119_b200.synth import preset_batch
     from paper_1911_00119_b200.trace import PackedEnvs
@@ -96,8 +96,10 @@ def build_workload(cfg: str, n_streams: int, n_steps: int, rank: int):
                                           overhead_budget=0.01 * ref))
     n_traces = 2048
     # scenario s -> (goal tuple s // 2048, trace s % 2048); a rank owns a contiguous range
-    s0 = rank * n_streams
-    scen = np.arange(s0, s0 + n_streams, dtype=np.int64)
+    # a rank's scenarios sample the whole 2^24 grid evenly (both modes, every
+    # goal tuple, every trace) when it holds fewer than 2^24 / world of them
+    stride = max(1, (1 << 24) // (n_streams * world))
+    scen = (rank * n_streams + np.arange(n_streams, dtype=np.int64)) * stride
     stream_spec = (scen // n_traces) % len(specs)
     stream_row = scen % n_traces
     parts = []
@@ -279,7 +281,7 @@ def main():
     from paper_1911_00119_b200.simulator import HostStreamer
 
     t0 = time.time()
-    wl = build_workload(args.config, S, N, rank)
+    wl = build_workload(args.config, S, N, rank, world)
     log(f"[rank {rank}] workload {args.config}: {S} streams x {N} steps built in {time.time() - t0:.1f}s")
     eng = A.get_engine(local)
     if args.lanes or args.tpb:
@@ -288,7 +290,14 @@ def main():
     C = table.n_candidates
     dev = eng.tdev
     trace = eng.upload_trace(wl["packed"], wl["stream_row"])
-    ss = None if wl["stream_spec"] is None else torch.as_tensor(wl["stream_spec"]).to(dev)
+    # one launch per contiguous run of one goal mode (mode-homogeneous kernels)
+    from paper_1911_00119_b200.packing import mode_runs
+
+    if wl["stream_spec"] is None:
+        launches = [(0, S, wl["specs"], None)]
+    else:
+        launches = [(b, e, sp, torch.as_tensor(full).to(dev)) for b, e, sp, full in mode_runs(wl["specs"],
+                                                                                           wl["stream_spec"])]
     agg = torch.zeros((S, abi.AGG_FIELDS), dtype=torch.float64, device=dev)
     rec = {}
     if args.records == "f32":
@@ -306,8 +315,9 @@ def main():
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        eng.run(table, wl["specs"], trace, state, policy=pol, stream_spec=ss, outputs=out, flags=args.flags,
-                stream_end=S)
+        for lb, le, lsp, lss in launches:
+            eng.run(table, lsp, trace, state, policy=pol, stream_spec=lss, outputs=out, flags=args.flags,
+                    stream_begin=lb, stream_end=le)
         if timed:
             b.record(stream)
             kev.append((a, b))

@@ -104,6 +104,33 @@ def z_quantile(p: float) -> float:
     return NormalDist().inv_cdf(p)
 
 
+def compact_specs(spec_arr: np.ndarray, stream_spec) -> tuple[np.ndarray, np.ndarray]:
+    """Keep only the specs some stream uses (stream_spec re-indexed): a launch
+    whose streams all minimise energy then gets the min-energy-only kernel
+    even when the caller's spec list also holds max-accuracy goals."""
+    ss = np.asarray(stream_spec, np.int64)
+    used, inv = np.unique(ss, return_inverse=True)
+    return np.ascontiguousarray(spec_arr[used]), inv.astype(np.int32).reshape(ss.shape)
+
+
+def mode_runs(spec_arr: np.ndarray, stream_spec) -> list[tuple[int, int, np.ndarray, np.ndarray]]:
+    """Split streams into maximal contiguous runs of one goal mode.  Each run
+    gets its own compacted spec list and a full-length stream_spec re-indexed
+    into it (entries outside the run are unused), so every launch sees a
+    mode-homogeneous spec set (min-energy-only kernel where possible)."""
+    ss = np.asarray(stream_spec, np.int64)
+    modes = spec_arr["mode"][ss]
+    cuts = np.flatnonzero(np.diff(modes)) + 1
+    bounds = [0, *cuts.tolist(), len(ss)]
+    runs = []
+    for b, e in zip(bounds[:-1], bounds[1:]):
+        used, inv = np.unique(ss[b:e], return_inverse=True)
+        full = np.zeros(len(ss), np.int32)
+        full[b:e] = inv.astype(np.int32)
+        runs.append((b, e, np.ascontiguousarray(spec_arr[used]), full))
+    return runs
+
+
 def pack_specs(specs: Sequence, group_sizes: Sequence[int | None] | int | None = None) -> np.ndarray:
     """ConstraintSpec objects -> AlertSpec records (validated like
     ConstraintSpec.__post_init__, model.py:81-97)."""

@@ -18,7 +18,7 @@ import numpy as np
 
 from . import abi
 from .engine import DeviceTrace, Engine, GpuTable, outputs_struct
-from .packing import pack_specs, policy_code
+from .packing import mode_runs, pack_specs, policy_code
 from .records import (
     RunResult, StepRecord, Summary, ViolationFlags, decision_of, summary_from_agg,
 )
@@ -90,9 +90,11 @@ def run_batch(space, specs: Sequence, envs, policy: str = "alert", *, kalman=Non
         len(stream_row) if stream_row is not None else trace.n_rows)
     steps = trace.n_steps
     dev = eng.tdev
-    ss = None
+    # launches: one per contiguous run of streams with one goal mode
     if stream_spec is not None:
-        ss = torch.as_tensor(np.asarray(stream_spec, np.int32)).to(dev)
+        launches = [(b, e, sp, torch.as_tensor(full).to(dev)) for b, e, sp, full in mode_runs(spec_arr, stream_spec)]
+    else:
+        launches = [(0, None, spec_arr, None)]
     state = eng.new_state(table, ns, kalman, idle_cfg)
     agg = torch.zeros((ns, abi.AGG_FIELDS), dtype=torch.float64, device=dev)
     rec = {}
@@ -117,8 +119,10 @@ def run_batch(space, specs: Sequence, envs, policy: str = "alert", *, kalman=Non
     if pol == abi.POLICY_ORACLE_STATIC:
         chunk = steps  # begin() is clairvoyant over the whole trace (policies.py:221-265)
     for s0 in range(0, steps, chunk):
-        eng.run(table, spec_arr, trace, state, policy=pol, kalman=kalman, idle_cfg=idle_cfg, stream_spec=ss,
-                outputs=out, flags=flags, stream_end=ns, step_begin=s0, step_end=min(steps, s0 + chunk))
+        for b, e, sp, ss in launches:
+            eng.run(table, sp, trace, state, policy=pol, kalman=kalman, idle_cfg=idle_cfg, stream_spec=ss,
+                    outputs=out, flags=flags, stream_begin=b, stream_end=ns if e is None else e, step_begin=s0,
+                    step_end=min(steps, s0 + chunk))
     if keep_on_device:
         return BatchResult(agg, state, rec, od, table.candidates)
     torch.cuda.synchronize(dev)
