@@ -76,6 +76,7 @@ enum { ALERT_DTYPE_F32 = 0, ALERT_DTYPE_F64 = 1 };
 #define ALERT_FLAG_NO_REFINE 0x2u  /* FP32 decision only (measures the refinement cost; not reference-exact) */
 #define ALERT_FLAG_NO_FAST 0x4u    /* disable the min-energy fast scan (full FP32 scan every step; A/B and tests) */
 #define ALERT_FLAG_FAST_ROWS 0x8u  /* fast scan in row mode even for small tables (tests) */
+#define ALERT_FLAG_ANY_WINDOW 0x10u /* anytime cells by the two-pass window instead of column skips (A/B, tests) */
 
 /* Compiled limits */
 #define ALERT_MAX_STAGES 8         /* stages per anytime DNN                   */

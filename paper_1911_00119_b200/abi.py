@@ -19,6 +19,7 @@ FLAG_FP64_ALL = 0x1
 FLAG_NO_REFINE = 0x2
 FLAG_NO_FAST = 0x4  # disable the min-energy fast scan (A/B, tests)
 FLAG_FAST_ROWS = 0x8  # fast scan in row mode (default for > 512 traditional cells)
+FLAG_ANY_WINDOW = 0x10  # anytime cells by the two-pass window (A/B, tests)
 MAX_STAGES = 8
 MAX_PHASES = 8
 MAX_CANDIDATES = 6144

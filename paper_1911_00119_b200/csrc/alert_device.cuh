@@ -175,6 +175,7 @@ struct StepCtx {
   const float4* sF;  // traditional cells {1/t, cap t, byte offset of the DNN's threshold in tT, 0}
   const float* zrow; // row mode (large tables): the spec's z' per traditional DNN (global, L1)
   const unsigned* wst;  // per 32-cell window of anytime cells: column-start bits (shared)
+  bool any_window;      // ALERT_FLAG_ANY_WINDOW: two-pass window for anytime cells (A/B)
   const int2* su;       // max-accuracy fast scan: units / key lower bounds staged in shared memory
   const float* slb;
   float hs, hm;      // T_d = fma(z'_d, hs, hm)
@@ -203,6 +204,7 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
   x.wst = nullptr;
   x.su = nullptr;
   x.slb = nullptr;
+  x.any_window = false;
   x.hs = x.hm = 0.f;
   x.Tpr = -kInfF;
   x.mu = mu;
@@ -733,7 +735,27 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
       if (HAS_PR) pen = fmaxf(pen, fmaf(mgH, A.x, x.Tpr));
       t.push(pack_key(A.y * fmax3(x.mu_e, fmaf(x.phig, A.x, x.ompmu), pen), k));
     };
-    if (W == 1) {
+    if (W == 1 && T.any_mono && !x.any_window) {
+      // One lane per stream, stage latencies non-decreasing: a column whose
+      // stage-0 energy-only key clears P2 (with the 4e-6 monotonicity margin)
+      // is skipped whole, and a column stops at its first such stage — per
+      // lane, no warp vote; usually no Phi at all (profiles/).
+      const float sc = 1.0f - 4e-6f;
+      const float mu_es = x.mu_e * sc, phigs = x.phig * sc, ompmus = x.ompmu * sc;
+      for (int col = 0; col < T.n_any_cols; ++col) {
+        const int2 cd = sCol[col];
+        const float4 A0 = sA[cd.x];
+        if (!(A0.y * fmaxf(mu_es, fmaf(phigs, A0.x, ompmus)) < t.p2)) continue;
+        float acc = A0.w;
+        for (int k = 0; k < cd.y; ++k) {
+          const float4 A = k == 0 ? A0 : sA[cd.x + k];
+          if (k > 0 && !(A.y * fmaxf(mu_es, fmaf(phigs, A.x, ompmus)) < t.p2)) break;
+          const float before = t.p1;
+          eval(A, acc, (unsigned)k);
+          if (t.p1 != before) t.blk = cd.x;
+        }
+      }
+    } else if (W == 1) {
       // One lane per stream: windows of 32 anytime cells.  Pass 1 (all cells,
       // independent): energy-only keys -> cells some lane of the warp needs
       // (key < P2); extended down to their column start (the Phi chain needs

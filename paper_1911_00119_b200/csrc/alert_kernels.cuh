@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
         x.fast = true;
         x.sF = sF;
         x.wst = sWst;
+        x.any_window = P.flags & ALERT_FLAG_ANY_WINDOW;
         if (P.units_smem) {
           x.su = sUn;
           x.slb = sLb;

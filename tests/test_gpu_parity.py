@@ -278,6 +278,9 @@ def test_fast_scan_equals_full_scan(seed):
                        lanes_per_stream=[1, 2, 4, 8][seed % 4], flags=abi.FLAG_NO_FAST)
     rows = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64,
                        lanes_per_stream=[1, 2, 4, 8][seed % 4], flags=abi.FLAG_FAST_ROWS)
+    win = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64,
+                      lanes_per_stream=[1, 2, 4, 8][seed % 4], flags=abi.FLAG_ANY_WINDOW)
+    np.testing.assert_array_equal(win.decoded()["cand"], full.decoded()["cand"])
     A.get_engine().set_launch(0, 0)
     np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
     np.testing.assert_array_equal(rows.decoded()["cand"], full.decoded()["cand"])
