@@ -889,8 +889,11 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
   const float mgH = -x.goal_f * kPenH;
   const float elH = -x.e_lo * kPenH;
   const int n_units = T.n_units;
-  const int2* __restrict__ sU = x.su;      // units staged in shared memory
-  const float* __restrict__ sLb = x.slb;
+  // units / key lower bounds: staged in shared memory for tables up to 1,024
+  // units, else read through L1 (read-only path)
+  const bool staged = x.su != nullptr;
+  auto unit_at = [&](int u) { return staged ? x.su[u] : __ldg(T.units + u); };
+  auto lb_at = [&](int u) { return staged ? x.slb[u] : __ldg(T.unit_lb + u); };
   // key of one cell, its energy and exact-one flag (running accuracy carried)
   auto cell_key = [&](const float4& A, float& acc, bool& one, unsigned k, float& E) {
     const float xz = fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s;
@@ -909,9 +912,9 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
   const bool store = W == 1 && x.has_sv;
   int u_end = lane;
   for (int u = lane; u < n_units; u += W) {
-    if (sLb[u] >= t.p2) break;
+    if (lb_at(u) >= t.p2) break;
     u_end = u + W;
-    const int2 un = sU[u];
+    const int2 un = unit_at(u);
     if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
     const int n = un.y & 0xFFFF;
     float acc = sA[un.x].w;
@@ -964,8 +967,8 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
     d.refined = false;
     return true;
   }
-  if (W == 1) {
-    // (c') one lane per stream: near-ties within P1's class (same DNN and
+  {
+    // (c') near-ties within P1's class (same DNN and
     // target stage) are ordered by the deadline-miss tail T = sum_m h_m d_m
     // (acc = a_k - T exactly; h_m = erfc(x_m) / 2, relatively accurate via
     // erfcf, 0 when x_m >= kExactOneX where FP64 rounds Pr to exactly 1):
@@ -976,9 +979,9 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
     bool ok1 = true;
     float ze1 = kInfF, ze2 = kInfF, bh = kInfF, bl = kInfF, lo2 = kInfF, nzlo = kInfF;
     int zc = -1, bc = -1;
-    for (int u = 0; u < n_units; ++u) {
-      if (sLb[u] > cut) break;
-      const int2 un = sU[u];
+    for (int u = lane; u < n_units; u += W) {
+      if (lb_at(u) > cut) break;
+      const int2 un = unit_at(u);
       if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
       int n = un.y & 0xFFFF;
       if (store && u < u_end) {  // keys kept by pass 1: the chain only up to the last key <= cut
@@ -1023,6 +1026,27 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
         }
       }
     }
+    // tile-wide merge: every lane ok; zero-tail energies (top-2 + cell);
+    // nonzero tails: best by upper bound, the smallest lower bound of the rest
+#pragma unroll
+    for (int m = 1; m < W; m <<= 1) {
+      ok1 = tile.shfl_xor((int)ok1, m) && ok1;
+      const float o1 = tile.shfl_xor(ze1, m), o2 = tile.shfl_xor(ze2, m);
+      const int oz = tile.shfl_xor(zc, m);
+      ze2 = fmin3(ze2, o2, fmaxf(ze1, o1));
+      if (o1 < ze1 || (o1 == ze1 && oz >= 0 && (zc < 0 || oz < zc))) zc = oz;
+      ze1 = fminf(ze1, o1);
+      const float obh = tile.shfl_xor(bh, m), obl = tile.shfl_xor(bl, m), olo2 = tile.shfl_xor(lo2, m);
+      const int obc = tile.shfl_xor(bc, m);
+      nzlo = fminf(nzlo, tile.shfl_xor(nzlo, m));
+      lo2 = fminf(lo2, olo2);
+      if (obh < bh || (obh == bh && obc >= 0 && (bc < 0 || obc < bc))) {
+        lo2 = fminf(lo2, bl);
+        bh = obh; bl = obl; bc = obc;
+      } else {
+        lo2 = fminf(lo2, obl);
+      }
+    }
     int w;
     if (!ok1) return false;
     if (zc >= 0) {  // zero tails win; nonzero ones must be strictly worse
@@ -1038,45 +1062,6 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
     d.refined = false;
     return true;
   }
-  // (c) near-tie: every key <= cut must be an exact-one cell of P1's class;
-  // the winner is then the lowest energy among them (re-scan of the few
-  // units that can reach the cut)
-  const int cls = cell_rank_a(sB[c1]);
-  int ok = 1;
-  float e1 = kInfF, e2 = kInfF;
-  int ce = -1;
-  for (int u = lane; u < n_units; u += W) {
-    if (sLb[u] > cut) break;
-    const int2 un = sU[u];
-    if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
-    const int n = un.y & 0xFFFF;
-    float acc = sA[un.x].w;
-    bool one = true;
-    for (int k = 0; k < n; ++k) {
-      float E;
-      const float key = cell_key(sA[un.x + k], acc, one, (unsigned)k, E);
-      if (key > cut) continue;
-      if (!one || cell_rank_a(sB[un.x + k]) != cls) ok = 0;
-      e2 = fminf(e2, fmaxf(e1, E));
-      if (E < e1) ce = un.x + k;
-      e1 = fminf(e1, E);
-    }
-  }
-  // tile-wide: all lanes ok, the lowest energy and its runner-up
-#pragma unroll
-  for (int m = 1; m < W; m <<= 1) {
-    const float o1 = tile.shfl_xor(e1, m), o2 = tile.shfl_xor(e2, m);
-    const int oc = tile.shfl_xor(ce, m);
-    ok &= tile.shfl_xor(ok, m);
-    e2 = fmin3(e2, o2, fmaxf(e1, o1));
-    if (o1 < e1 || (o1 == e1 && oc >= 0 && (ce < 0 || oc < ce))) ce = oc;
-    e1 = fminf(e1, o1);
-  }
-  if (!ok || ce < 0 || ce >= T.n_cells || !(e2 > e1 + e1 * (4.0f * x.d_erel) + 1e-30f) || !sure(ce)) return false;
-  d.cell = ce;
-  d.level = 0;
-  d.refined = false;
-  return true;
 }
 
 // Re-rank pass from the stored FP32 objectives (no re-scan): the same
@@ -1219,7 +1204,7 @@ __device__ __forceinline__ Decision alert_decide_t(const DevTable& T, const floa
     if (ok) return d;
     tried = true;
   }
-  if (MODE == ALERT_MODE_MAX_ACCURACY && x.fast && !x.fp64_all && x.su) {
+  if (MODE == ALERT_MODE_MAX_ACCURACY && x.fast && !x.fp64_all && T.units) {
     const unsigned am = __activemask();
     Decision d{-1, 0, false};
     const bool ok = fast_max_accuracy<HAS_PR>(T, sA, sB, tile, x, kinds, d);
