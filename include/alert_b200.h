@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define ALERT_ABI_VERSION 1
+#define ALERT_ABI_VERSION 2  /* 2: comparison-scheme policies, AlertSpaceDesc.sys_dnn/app_dnn, AlertState.policy_aux, AlertOutputs.fb_*, alert_xi_stats */
 
 /* ---- status codes ------------------------------------------------------ */
 typedef enum AlertStatus {
@@ -220,6 +220,8 @@ typedef struct AlertOutputs {
   double* agg;          /* [n_streams][ALERT_AGG_FIELDS] or NULL */
   const int32_t* forced; /* [step][stream] candidate to execute (teacher
                             forcing) or -1; NULL = free running.  Same strides. */
+  double* fb_latency;   /* StepRecord.fb_latency (FP64, same strides) or NULL */
+  double* fb_t_prof;    /* StepRecord.fb_t_prof  (FP64, same strides) or NULL */
 } AlertOutputs;
 
 /* One prediction (predictor.Prediction, predictor.py:36-45), FP64. */
@@ -300,6 +302,15 @@ int64_t alert_launch_count(AlertContext* ctx);
 /* Measured FP32 issue peak (FFMA lane-ops/s) of a device: the denominator of
  * the FP32 roofline (instrumentation, not part of the scheduling path). */
 int alert_probe_fp32_peak(int device, double* slots_per_s);
+
+/* xi_diagnostics_from_values (simulator.py:521-543): xi = num / den (den may be
+ * NULL: xi = num), n >= 1 values, DEVICE buffers.  counts[bins] / edges[bins+1]
+ * follow numpy.histogram(xi, bins) bit for bit (min/max edges, linspace,
+ * numpy's index correction); mean_sd[2] = numpy.mean / numpy.std with numpy's
+ * pairwise summation order.  (The reference needs >= 30 values; the caller
+ * checks, as the reference raises ValueError.) */
+int alert_xi_stats(AlertContext* ctx, const double* num, const double* den, int64_t n, int32_t bins,
+                   int64_t* counts, double* edges, double* mean_sd, void* cuda_stream);
 
 /* The scan's FP32 normal CDF: out[i] = Phi(sqrt(2) * x[i]) for device arrays
  * (instrumentation: lets tests bound its error against FP64). */

@@ -7,6 +7,7 @@ scheduling arithmetic runs in libalert_b200.so (hand-written sm_100a CUDA);
 there is no CPU fallback.
 """
 
+from .diagnostics import XiDiagnostics, xi_diagnostics, xi_diagnostics_from_values
 from .estimator import IdleFilterConfig, IdlePowerEstimate, KalmanConfig, SlowdownEstimate, idle_power_init, slowdown_init
 from .model import ConfigSpace, ConstraintSpec, DnnKind, DnnProfile, Mode, PowerSetting, Stage, fastest_dnn, validate
 from .packing import ProfileError, pack_space, pack_specs

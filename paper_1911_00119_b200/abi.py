@@ -6,7 +6,7 @@ import ctypes as C
 
 import numpy as np
 
-ALERT_ABI_VERSION = 1
+ALERT_ABI_VERSION = 2
 
 KIND_TRADITIONAL, KIND_ANYTIME = 0, 1
 MODE_MIN_ENERGY, MODE_MAX_ACCURACY = 0, 1
@@ -123,6 +123,7 @@ class AlertOutputs(C.Structure):
         ("oracle_decision", C.c_void_p), ("record_dtype", C.c_int32), ("_pad", C.c_int32),
         ("stream_stride", C.c_int64), ("step_stride", C.c_int64),
         ("agg", C.c_void_p), ("forced", C.c_void_p),
+        ("fb_latency", C.c_void_p), ("fb_t_prof", C.c_void_p),
     ]
 
 

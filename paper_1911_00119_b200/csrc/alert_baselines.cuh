@@ -257,6 +257,11 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
       count -= 1;
     }
     const AlertOutputs& out = P.out;
+    if (out.fb_latency) {
+      const long long oidx = stream * out.stream_stride + n * out.step_stride;
+      out.fb_latency[oidx] = o.fb_latency;
+      out.fb_t_prof[oidx] = o.fb_t_prof;
+    }
     if (out.decision) {
       const long long oidx = stream * out.stream_stride + n * out.step_stride;
       out.decision[oidx] = pack_decision(cell_cand(T.cellB[cell]), 0, o, false, phase);

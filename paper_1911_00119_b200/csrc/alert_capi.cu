@@ -139,6 +139,117 @@ __global__ void zlo_kernel(const SpecDev* specs, int n_specs, const Cell64* c64,
   out[i] = fmaf(-20.0f * kEps, fabsf(zf), zf);
 }
 
+
+// ==========================================================================
+// xi diagnostics (simulator.py:521-543): numpy.histogram(xi, 40) + mean / std
+// with numpy's exact arithmetic (linspace edges, index correction, pairwise
+// summation order; see alert_xi_stats).
+__device__ __forceinline__ double xi_at(const double* num, const double* den, long long i) {
+  return den ? xdiv(num[i], den[i]) : num[i];
+}
+
+__global__ void xi_minmax_kernel(const double* num, const double* den, long long n, int bins, double* edges,
+                                 double* scratch) {
+  __shared__ double smin[1024], smax[1024];
+  double mn = kInf, mx = -kInf;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = xi_at(num, den, i);
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  smin[threadIdx.x] = mn;
+  smax[threadIdx.x] = mx;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + w]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double first = smin[0], last = smax[0];
+    if (first == last) {  // _get_outer_edges: expand an empty range
+      first = xsub(first, 0.5);
+      last = xadd(last, 0.5);
+    }
+    // np.linspace(first, last, bins + 1): y = arange * step + start, y[-1] = stop
+    const double delta = xsub(last, first), step = xdiv(delta, (double)bins);
+    for (int i = 0; i < bins; ++i)
+      edges[i] = step == 0.0 ? xadd(xmul(xdiv((double)i, (double)bins), delta), first)
+                             : xadd(xmul((double)i, step), first);
+    edges[bins] = last;
+    scratch[0] = first;
+    scratch[1] = last;
+  }
+}
+
+__global__ void xi_hist_kernel(const double* num, const double* den, long long n, int bins, const double* edges,
+                               const double* scratch, unsigned long long* counts) {
+  const double first = scratch[0], last = scratch[1];
+  const double denom = xsub(last, first);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double v = xi_at(num, den, i);
+    if (!(v >= first && v <= last)) continue;
+    long long k = (long long)xmul(xdiv(xsub(v, first), denom), (double)bins);
+    if (k == bins) k -= 1;
+    if (v < edges[k]) k -= 1;
+    if (v >= edges[k + 1] && k != bins - 1) k += 1;
+    atomicAdd(counts + k, 1ull);
+  }
+}
+
+// numpy's pairwise_sum (loops_utils.h) on one leaf (n <= 128)
+__device__ double np_leaf_sum(const double* num, const double* den, long long off, long long n, int mode,
+                              double mean) {
+  auto val = [&](long long i) {
+    const double v = xi_at(num, den, off + i);
+    if (mode == 0) return v;
+    const double d = xsub(v, mean);
+    return xmul(d, d);
+  };
+  if (n < 8) {
+    double res = 0.0;
+    for (long long i = 0; i < n; ++i) res = xadd(res, val(i));
+    return res;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = val(j);
+  long long i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = xadd(r[j], val(i + j));
+  double res = xadd(xadd(xadd(r[0], r[1]), xadd(r[2], r[3])), xadd(xadd(r[4], r[5]), xadd(r[6], r[7])));
+  for (; i < n; ++i) res = xadd(res, val(i));
+  return res;
+}
+
+__global__ void xi_leaf_kernel(const double* num, const double* den, const long long* leaves, int n_leaves, int mode,
+                               const double* mean_sd, double* leaf_sums) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_leaves) return;
+  leaf_sums[k] = np_leaf_sum(num, den, leaves[2 * k], leaves[2 * k + 1], mode, mode ? mean_sd[0] : 0.0);
+}
+
+// replays the pairwise recursion: prog = post-order of leaf pushes (>= 0)
+// and additions (-1); mode 0 -> mean, mode 1 -> sd
+__global__ void xi_combine_kernel(const int* prog, int n_prog, const double* leaf_sums, long long n, int mode,
+                                  double* mean_sd) {
+  double stack[80];
+  int sp = 0;
+  for (int i = 0; i < n_prog; ++i) {
+    const int op = prog[i];
+    if (op >= 0) {
+      stack[sp++] = leaf_sums[op];
+    } else {
+      const double b = stack[--sp], a = stack[--sp];
+      stack[sp++] = xadd(a, b);
+    }
+  }
+  const double q = xdiv(stack[0], (double)n);
+  if (mode == 0) mean_sd[0] = q;
+  else mean_sd[1] = sqrt(q);
+}
+
 __global__ void state_init_kernel(AlertState st, AlertFilterConfig cfg, double phi0, long long n) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -959,3 +1070,52 @@ int alert_reduce(AlertContext* ctx, const double* agg, int64_t n, double* out, v
   return ALERT_OK;
 }
 
+// numpy pairwise_sum recursion (n > 128: split at n/2 rounded down to a
+// multiple of 8) as leaves + a post-order program
+static void np_pairwise_plan(long long off, long long n, std::vector<long long>& leaves, std::vector<int>& prog) {
+  if (n <= 128) {
+    prog.push_back((int)(leaves.size() / 2));
+    leaves.push_back(off);
+    leaves.push_back(n);
+    return;
+  }
+  long long n2 = n / 2;
+  n2 -= n2 % 8;
+  np_pairwise_plan(off, n2, leaves, prog);
+  np_pairwise_plan(off + n2, n - n2, leaves, prog);
+  prog.push_back(-1);
+}
+
+int alert_xi_stats(AlertContext* ctx, const double* num, const double* den, int64_t n, int32_t bins,
+                   int64_t* counts, double* edges, double* mean_sd, void* cuda_stream) {
+  if (!ctx || !num || !counts || !edges || !mean_sd) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_xi_stats: NULL argument");
+  if (n < 1 || bins < 1) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_xi_stats: need n >= 1 values and bins >= 1");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  std::vector<long long> leaves;
+  std::vector<int> prog;
+  np_pairwise_plan(0, n, leaves, prog);
+  const int n_leaves = (int)(leaves.size() / 2);
+  char* buf = nullptr;
+  const size_t b_leaves = sizeof(long long) * leaves.size(), b_prog = sizeof(int) * prog.size();
+  const size_t bytes = b_leaves + b_prog + sizeof(double) * (size_t)n_leaves + 2 * sizeof(double) + 64;
+  CUDA_TRY(cudaMallocAsync((void**)&buf, bytes, s));
+  long long* d_leaves = reinterpret_cast<long long*>(buf);
+  int* d_prog = reinterpret_cast<int*>(buf + b_leaves);
+  double* d_sums = reinterpret_cast<double*>(buf + ((b_leaves + b_prog + 15) & ~size_t(15)));
+  double* d_scr = d_sums + n_leaves;
+  CUDA_TRY(cudaMemcpyAsync(d_leaves, leaves.data(), b_leaves, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_prog, prog.data(), b_prog, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int64_t) * bins, s));
+  xi_minmax_kernel<<<1, 1024, 0, s>>>(num, den, n, bins, edges, d_scr);
+  xi_hist_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 8), 256, 0, s>>>(
+      num, den, n, bins, edges, d_scr, reinterpret_cast<unsigned long long*>(counts));
+  for (int mode = 0; mode < 2; ++mode) {
+    xi_leaf_kernel<<<(n_leaves + 127) / 128, 128, 0, s>>>(num, den, d_leaves, n_leaves, mode, mean_sd, d_sums);
+    xi_combine_kernel<<<1, 1, 0, s>>>(d_prog, (int)prog.size(), d_sums, n, mode, mean_sd);
+  }
+  CUDA_TRY(cudaGetLastError());
+  cudaFreeAsync(buf, s);
+  ctx->launches += 6;
+  return ALERT_OK;
+}

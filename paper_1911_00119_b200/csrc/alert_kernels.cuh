@@ -391,6 +391,11 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       cs.count -= 1;
     }
     const AlertOutputs& out = P.out;
+    if (writer && out.fb_latency) {  // StepRecord feedback pair (xi diagnostics)
+      const long long oidx = stream_ll * out.stream_stride + (long long)n * out.step_stride;
+      out.fb_latency[oidx] = o.fb_latency;
+      out.fb_t_prof[oidx] = o.fb_t_prof;
+    }
     if (writer && out.decision) {
       const long long oidx = stream_ll * out.stream_stride + (long long)n * out.step_stride;
       out.decision[oidx] = pack_decision(cell_cand(sB[d.cell]), d.level, o, d.refined, cs.phase);

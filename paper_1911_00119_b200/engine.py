@@ -251,4 +251,7 @@ def outputs_struct(records: dict | None = None, agg=None, forced=None, oracle_de
         out.stream_stride = ref.stride(1)
     if agg is not None:
         out.agg = agg.data_ptr()
+    if records and records.get("fb_latency") is not None:
+        out.fb_latency = records["fb_latency"].data_ptr()
+        out.fb_t_prof = records["fb_t_prof"].data_ptr()
     return out

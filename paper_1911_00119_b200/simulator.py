@@ -103,6 +103,9 @@ def run_batch(space, specs: Sequence, envs, policy: str = "alert", *, kalman=Non
         rec["decision"] = torch.empty((steps, ns), dtype=torch.int32, device=dev)
         for k in ("energy", "accuracy", "latency", "mu", "sigma2"):
             rec[k] = torch.empty((steps, ns), dtype=vdt, device=dev)
+        if records == "f64":  # StepRecord feedback pair (fb_latency, fb_t_prof)
+            for k in ("fb_latency", "fb_t_prof"):
+                rec[k] = torch.empty((steps, ns), dtype=torch.float64, device=dev)
     pol = policy_code(policy)
     od = None
     if pol == abi.POLICY_ALERT_WITH_ORACLE and records:
@@ -245,6 +248,7 @@ def run(space, spec, trace, policy) -> RunResult:
             violations=ViolationFlags(bool(d["viol_lat"][n, 0]), bool(d["viol_acc"][n, 0]),
                                       bool(d["viol_energy"][n, 0])),
             phase_index=int(env.phase_index[n]), idle_power_true=float(env.idle_power[n]),
+            fb_latency=float(res.records["fb_latency"][n, 0]), fb_t_prof=float(res.records["fb_t_prof"][n, 0]),
         ))
     return RunResult(tuple(recs), summary_from_agg(res.agg[0], len(trace.phases)))
 
