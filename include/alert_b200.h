@@ -303,6 +303,25 @@ int64_t alert_launch_count(AlertContext* ctx);
  * the FP32 roofline (instrumentation, not part of the scheduling path). */
 int alert_probe_fp32_peak(int device, double* slots_per_s);
 
+/* On-device trace realization: one stream per
+ * thread, Philox4x32-10 (curand) keyed by (seed, stream_offset + stream), the
+ * reference's per-phase recipe (simulator.py:221-235: draw from the phase's
+ * distribution, multiply by N(1, input_noise_sd) when > 0, floor at 0.01).
+ * The VALUES differ from numpy's PCG64 streams (distributional parity only);
+ * decisions are checked against the CPU oracle on the exported arrays.
+ * out: time-major [sum(length)][n_streams] with row stride n_streams, FP32
+ * (dtype ALERT_DTYPE_F32) or FP64. */
+enum { ALERT_DIST_CONSTANT = 0, ALERT_DIST_GAUSSIAN = 1, ALERT_DIST_LOGNORMAL = 2, ALERT_DIST_UNIFORM = 3 };
+typedef struct AlertPhaseDesc {
+  int64_t length;
+  int32_t dist;          /* ALERT_DIST_* */
+  int32_t _pad;
+  double a, b;           /* Constant: value; Gaussian: mean, sd; LogNormal: mu_log, sd_log; Uniform: lo, hi */
+  double input_noise_sd;
+} AlertPhaseDesc;
+int alert_realize(AlertContext* ctx, const AlertPhaseDesc* phases, int32_t n_phases, uint64_t seed,
+                  int64_t stream_offset, int64_t n_streams, void* out, int32_t dtype, void* cuda_stream);
+
 /* xi_diagnostics_from_values (simulator.py:521-543): xi = num / den (den may be
  * NULL: xi = num), n >= 1 values, DEVICE buffers.  counts[bins] / edges[bins+1]
  * follow numpy.histogram(xi, bins) bit for bit (min/max edges, linspace,

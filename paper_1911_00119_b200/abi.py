@@ -158,3 +158,11 @@ def decode_decision(word):
         "refined": ((w >> 26) & 1).astype(np.int32),
         "phase": ((w >> 27) & 0x7).astype(np.int32),
     }
+
+
+DIST_CONSTANT, DIST_GAUSSIAN, DIST_LOGNORMAL, DIST_UNIFORM = range(4)
+
+
+class AlertPhaseDesc(C.Structure):
+    _fields_ = [("length", C.c_int64), ("dist", C.c_int32), ("_pad", C.c_int32), ("a", C.c_double),
+                ("b", C.c_double), ("input_noise_sd", C.c_double)]

@@ -12,6 +12,8 @@
 
 #include "alert_baselines.cuh"
 
+#include <curand_kernel.h>
+
 using namespace alert;
 
 // ==========================================================================
@@ -1117,5 +1119,54 @@ int alert_xi_stats(AlertContext* ctx, const double* num, const double* den, int6
   CUDA_TRY(cudaGetLastError());
   cudaFreeAsync(buf, s);
   ctx->launches += 6;
+  return ALERT_OK;
+}
+
+// On-device realization (simulator.py:221-235 recipe, Philox streams).
+__global__ void realize_kernel(const AlertPhaseDesc* ph, int n_ph, unsigned long long seed, long long off,
+                               long long n, void* out, int f64) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  curandStatePhilox4_32_10_t rs;
+  curand_init(seed, (unsigned long long)(off + k), 0ull, &rs);
+  long long step = 0;
+  for (int p = 0; p < n_ph; ++p) {
+    const AlertPhaseDesc d = ph[p];
+    for (long long i = 0; i < d.length; ++i, ++step) {
+      double s;
+      switch (d.dist) {
+        case ALERT_DIST_CONSTANT: s = d.a; break;
+        case ALERT_DIST_GAUSSIAN: s = d.a + d.b * curand_normal_double(&rs); break;
+        case ALERT_DIST_LOGNORMAL: s = exp(d.a + d.b * curand_normal_double(&rs)); break;
+        default: s = d.a + (d.b - d.a) * curand_uniform_double(&rs); break;
+      }
+      if (d.input_noise_sd > 0.0) s *= 1.0 + d.input_noise_sd * curand_normal_double(&rs);
+      s = fmax(s, 0.01);  // MIN_SLOWDOWN, simulator.py:28
+      if (f64) static_cast<double*>(out)[step * n + k] = s;
+      else static_cast<float*>(out)[step * n + k] = (float)s;
+    }
+  }
+}
+
+int alert_realize(AlertContext* ctx, const AlertPhaseDesc* phases, int32_t n_phases, uint64_t seed,
+                  int64_t stream_offset, int64_t n_streams, void* out, int32_t dtype, void* cuda_stream) {
+  if (!ctx || !phases || !out || n_phases < 1) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_realize: bad argument");
+  if (dtype != ALERT_DTYPE_F32 && dtype != ALERT_DTYPE_F64)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_realize: unknown dtype");
+  for (int p = 0; p < n_phases; ++p)
+    if (phases[p].length < 0 || phases[p].dist < 0 || phases[p].dist > ALERT_DIST_UNIFORM)
+      return fail(ALERT_ERR_INVALID_TRACE, "alert_realize: bad phase description");
+  if (n_streams <= 0) return n_streams < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_realize: n < 0") : ALERT_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  AlertPhaseDesc* d = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&d, sizeof(AlertPhaseDesc) * n_phases, s));
+  CUDA_TRY(cudaMemcpyAsync(d, phases, sizeof(AlertPhaseDesc) * n_phases, cudaMemcpyHostToDevice, s));
+  realize_kernel<<<(unsigned)((n_streams + 127) / 128), 128, 0, s>>>(d, n_phases, seed, stream_offset, n_streams, out,
+                                                                    dtype == ALERT_DTYPE_F64);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(d, s);
+  if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("realize_kernel: ") + cudaGetErrorString(e));
+  ctx->launches++;
   return ALERT_OK;
 }

@@ -169,3 +169,55 @@ def preset_batch(n_streams: int, lengths=(3334, 3333, 3333), seed0: int = 42, in
         seg_phase=np.tile(np.arange(nseg, dtype=np.int32), (n_streams, 1)),
         seg_idle=np.tile(np.array([regimes_idle[r] for r in order], np.float64), (n_streams, 1)),
     )
+
+
+def realize_on_device(phases, n_streams: int, seed: int = 42, stream_offset: int = 0, dtype=np.float32,
+                      device: int = 0):
+    """Traces for many streams generated ON THE GPU:
+    the reference's per-phase recipe (simulator.py:221-235 — draw, optional
+    N(1, input_noise_sd) jitter, floor at 0.01) with Philox4x32-10 streams
+    keyed by (seed, stream index).  Returns a DeviceTrace (time-major, never
+    copied to the host).  The values are NOT numpy's PCG64 draws: parity is
+    distributional, and decisions are checked on exported arrays
+    (``trace.slowdown.cpu()``) against the CPU oracle."""
+    import ctypes as C
+
+    import torch
+
+    from . import abi
+    from ._lib import check, load
+    from .engine import DeviceTrace
+    from .simulator import get_engine
+    from .trace import Constant, Gaussian, LogNormal, Uniform
+
+    eng = get_engine(device)
+    descs = (abi.AlertPhaseDesc * len(phases))()
+    for k, p in enumerate(phases):
+        d = p.slowdown_dist
+        if isinstance(d, Constant) or type(d).__name__ == "Constant":
+            kind, a, b = abi.DIST_CONSTANT, d.value, 0.0
+        elif type(d).__name__ == "Gaussian":
+            kind, a, b = abi.DIST_GAUSSIAN, d.mean_, d.sd
+        elif type(d).__name__ == "LogNormal":
+            kind, a, b = abi.DIST_LOGNORMAL, d.mu_log, d.sd_log
+        elif type(d).__name__ == "Uniform":
+            kind, a, b = abi.DIST_UNIFORM, d.lo, d.hi
+        else:
+            raise ValueError(f"unknown slow-down distribution {d!r}")
+        descs[k] = abi.AlertPhaseDesc(int(p.length), kind, 0, float(a), float(b), float(p.input_noise_sd))
+    steps = sum(int(p.length) for p in phases)
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    out = torch.empty((steps, n_streams), dtype=tdt, device=eng.tdev)
+    check(load().alert_realize(eng.ctx, descs, len(phases), int(seed), int(stream_offset), int(n_streams),
+                               out.data_ptr(), abi.DTYPE_F64 if dtype == np.float64 else abi.DTYPE_F32,
+                               eng._stream()))
+    ends = np.cumsum([int(p.length) for p in phases]).astype(np.int32)
+    d = eng.tdev
+    nseg = len(phases)
+    return DeviceTrace(
+        slowdown=out,
+        n_segments=torch.full((n_streams,), nseg, dtype=torch.int32, device=d),
+        seg_end=torch.as_tensor(np.tile(ends, (n_streams, 1))).to(d),
+        seg_phase=torch.as_tensor(np.tile(np.arange(nseg, dtype=np.int32), (n_streams, 1))).to(d),
+        seg_idle=torch.as_tensor(np.tile(np.array([float(p.idle_power_true) for p in phases]), (n_streams, 1))).to(d),
+    )
