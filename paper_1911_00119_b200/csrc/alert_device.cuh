@@ -93,13 +93,15 @@ __device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a,
 __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
 __device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
 
-// Neumaier step exactly as CPython 3.12 sum() (bltinmodule.c).
+// Neumaier step exactly as CPython 3.12 sum() (bltinmodule.c): its
+// correction (s - t) + x or (x - t) + s is the EXACT rounding error of s + x
+// (Fast2Sum on the larger operand), which TwoSum yields without the compare
+// and selects — bit-identical, shorter dependency chain.
 __device__ __forceinline__ void neumaier(double& s, double& c, double x) {
-  double t = xadd(s, x);
-  if (fabs(s) >= fabs(x))
-    c = xadd(c, xadd(xsub(s, t), x));
-  else
-    c = xadd(c, xadd(xsub(x, t), s));
+  const double t = xadd(s, x);
+  const double bp = xsub(t, s);
+  const double ap = xsub(t, bp);
+  c = xadd(c, xadd(xsub(s, ap), xsub(x, bp)));
   s = t;
 }
 
@@ -612,14 +614,12 @@ __device__ __forceinline__ void fast_prep(StepCtx& x, const Tile& tile, const fl
     x.zrow = zrow;
     return;
   }
-  const int step = Tile::num_threads() * tS;
-  const float* zp = zt + tile.thread_rank() * tS;
-  float* tp = tT + tile.thread_rank() * tS;
-  for (int d = tile.thread_rank(); d < n_tdnn; d += Tile::num_threads(), zp += step, tp += step)
-    *tp = fmaf(*zp, x.hs, x.hm);
-  x.tT = tT;
+  // flat mode: the scan forms T_d = fma(z'_d, hs, hm) per cell from the
+  // tile's z' copy (one FFMA; no per-step table, no store -> load dependency)
+  (void)tT;
+  (void)n_tdnn;
+  x.tT = zt;
   x.tS = tS;
-  if (Tile::num_threads() > 1) tile.sync();
 }
 
 // FP32 sureness of one cell at min-energy level 0 (the full scan's margins).
@@ -678,7 +678,7 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
     const char* tb = reinterpret_cast<const char*>(x.tT);
     const float4* sF = x.sF;
     auto key_of = [&](const float4& F) {  // F.w = the cell's position in its chunk
-      const float Td = *reinterpret_cast<const float*>(tb + __float_as_int(F.z));
+      const float Td = fmaf(*reinterpret_cast<const float*>(tb + __float_as_int(F.z)), x.hs, x.hm);
       return pack_key(F.y * fmax3(x.mu_e, fmaf(x.phig, F.x, x.ompmu), fmaf(mgH, F.x, Td)), __float_as_uint(F.w));
     };
     const int n = T.n_trad;
