@@ -334,6 +334,8 @@ int alert_xi_stats(AlertContext* ctx, const double* num, const double* den, int6
 /* The scan's FP32 normal CDF: out[i] = Phi(sqrt(2) * x[i]) for device arrays
  * (instrumentation: lets tests bound its error against FP64). */
 int alert_probe_phi32(const float* x, float* out, int64_t n, void* cuda_stream);
+/* erfc(x) with relative accuracy (max-accuracy tail ordering), instrumentation. */
+int alert_probe_erfc_rel(const float* x, float* out, int64_t n, void* cuda_stream);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,7 @@ EXPORTS = (
     "alert_table_create", "alert_table_destroy", "alert_table_num_candidates", "alert_table_candidate",
     "alert_state_init", "alert_run", "alert_decide", "alert_predict", "alert_observe",
     "alert_oracle_decide", "alert_reduce", "alert_set_launch", "alert_get_launch", "alert_launch_count",
-    "alert_probe_fp32_peak", "alert_probe_phi32", "alert_xi_stats", "alert_realize",
+    "alert_probe_fp32_peak", "alert_probe_phi32", "alert_xi_stats", "alert_realize", "alert_probe_erfc_rel",
 )
 
 
@@ -66,6 +66,7 @@ def load() -> C.CDLL:
     L.alert_launch_count.restype = C.c_int64
     L.alert_probe_fp32_peak.argtypes = [C.c_int, P(C.c_double)]
     L.alert_probe_phi32.argtypes = [V, V, C.c_int64, V]
+    L.alert_probe_erfc_rel.argtypes = [V, V, C.c_int64, V]
     L.alert_xi_stats.argtypes = [V, V, V, C.c_int64, C.c_int32, V, V, V, V]
     L.alert_realize.argtypes = [V, V, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, V, C.c_int32, V]
     if L.alert_abi_version() != abi.ALERT_ABI_VERSION:

@@ -880,6 +880,24 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
 // Otherwise the full scan runs.
 constexpr float kExactOneX = 6.0811183f;  // z = 8.6 in units of z / sqrt 2
 
+// erfc(x) for 0 <= x < ~9 with RELATIVE accuracy (Chebyshev-fitted
+// exponent form, fractional error < 1.2e-7 in exact arithmetic; FP32
+// evaluation adds a few ulp of the exponent): t = 1/(1 + x/2),
+// erfc = t exp(-x^2 + P(t)).  ~14 instructions vs erfcf's ~50.
+__device__ __forceinline__ float erfc_rel(float x) {
+  const float t = rcp_approx(fmaf(0.5f, x, 1.0f));
+  float p = fmaf(t, 0.17087277f, -0.82215223f);
+  p = fmaf(t, p, 1.48851587f);
+  p = fmaf(t, p, -1.13520398f);
+  p = fmaf(t, p, 0.27886807f);
+  p = fmaf(t, p, -0.18628806f);
+  p = fmaf(t, p, 0.09678418f);
+  p = fmaf(t, p, 0.37409196f);
+  p = fmaf(t, p, 1.00002368f);
+  p = fmaf(t, p, -1.26551223f);
+  return t * ex2_approx(fmaf(-x, x, p) * 1.44269504088896341f);
+}
+
 template <bool HAS_PR, class Tile>
 __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float4* __restrict__ sA,
                                                   const float4* __restrict__ sB, const Tile& tile,
@@ -1003,9 +1021,11 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
         const float key = cell_key(A, acc, one, (unsigned)k, E);
         if (!(xz >= kExactOneX)) {
           bad |= !(xz >= 0.0f) || !(A.z >= 0.0f);
-          tail = fmaf(0.5f * erfcf(xz), A.z, tail);
+          tail = fmaf(0.5f * erfc_rel(xz), A.z, tail);
+          // relative error: FP32 x (propagated by d ln erfc / dx ~ 2x + 2),
+          // the fit (1.2e-7) and the FP32 exponent (<= 40 ulp of 1 at x ~ 6)
           const float dx = 4.0f * kEps * (fmaf(x.goal_f, A.x, fabsf(x.mu_f)) * x.inv_sig_s + fabsf(xz));
-          r = fmaxf(r, fmaf(2.0f * xz + 2.0f, dx, 1e-5f));
+          r = fmaxf(r, fmaf(2.0f * xz + 2.0f, dx, 1e-4f));
         }
         if (key > cut) continue;
         const int c = un.x + k;

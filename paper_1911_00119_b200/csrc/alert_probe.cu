@@ -65,3 +65,17 @@ int alert_probe_phi32(const float* x, float* out, int64_t n, void* cuda_stream) 
   phi32_probe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)cuda_stream>>>(x, out, n);
   return cudaGetLastError() == cudaSuccess ? ALERT_OK : ALERT_ERR_CUDA;
 }
+
+__global__ void erfc_rel_probe_kernel(const float* x, float* out, long long n) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = alert::erfc_rel(x[i]);
+}
+
+// The relatively accurate FP32 erfc of the max-accuracy tail ordering ->
+// out[i] (device pointers): lets the tests bound its RELATIVE error.
+int alert_probe_erfc_rel(const float* x, float* out, int64_t n, void* cuda_stream) {
+  if (!x || !out || n < 0) return ALERT_ERR_INVALID_ARGUMENT;
+  if (n == 0) return ALERT_OK;
+  erfc_rel_probe_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)cuda_stream>>>(x, out, n);
+  return cudaGetLastError() == cudaSuccess ? ALERT_OK : ALERT_ERR_CUDA;
+}

@@ -451,3 +451,22 @@ def test_oracle_fp32_scan_equals_fp64(seed):
         np.testing.assert_array_equal(fast.agg[:, abi.AGG_PHASE_BASE:], full.agg[:, abi.AGG_PHASE_BASE:])
         if policy == "alert+oracle":
             np.testing.assert_array_equal(fast.oracle_decision & 0xFFFF, full.oracle_decision & 0xFFFF)
+
+
+def test_erfc_rel_relative_error_bound():
+    """The tail ordering's FP32 erfc: relative error vs FP64 erfc stays well
+    inside the 1e-4 floor of its margin over [0, 6.1] (below kExactOneX)."""
+    import math
+
+    from paper_1911_00119_b200._lib import load
+
+    xs = np.concatenate([np.linspace(0.0, 6.1, 400001), np.random.default_rng(1).uniform(0, 6.1, 100000)])
+    x = torch.tensor(xs, dtype=torch.float32, device="cuda")
+    out = torch.empty_like(x)
+    assert load().alert_probe_erfc_rel(x.data_ptr(), out.data_ptr(), x.numel(), None) == 0
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().astype(np.float64)
+    xf = x.cpu().numpy().astype(np.float64)  # the FP32 argument the kernel saw
+    ref = np.array([math.erfc(v) for v in xf])
+    rel = np.abs(got / ref - 1.0)
+    assert rel.max() < 5e-5, rel.max()
