@@ -96,10 +96,11 @@ def build_workload(cfg: str, n_streams: int, n_steps: int, rank: int, world: int
                                           overhead_budget=0.01 * ref))
     n_traces = 2048
     # scenario s -> (goal tuple s // 2048, trace s % 2048); a rank owns a contiguous range
-    # a rank's scenarios sample the whole 2^24 grid evenly (both modes, every
-    # goal tuple, every trace) when it holds fewer than 2^24 / world of them
+    # every rank's scenarios sample the whole 2^24 grid evenly (both modes,
+    # every goal tuple, every trace; ranks interleaved, disjoint) when the job
+    # holds fewer than 2^24 of them
     stride = max(1, (1 << 24) // (n_streams * world))
-    scen = (rank * n_streams + np.arange(n_streams, dtype=np.int64)) * stride
+    scen = (np.arange(n_streams, dtype=np.int64) * world + rank) * stride
     stream_spec = (scen // n_traces) % len(specs)
     stream_row = scen % n_traces
     parts = []
