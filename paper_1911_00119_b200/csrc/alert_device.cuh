@@ -991,9 +991,13 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
     // (acc = a_k - T exactly; h_m = erfc(x_m) / 2, relatively accurate via
     // erfcf, 0 when x_m >= kExactOneX where FP64 rounds Pr to exactly 1):
     // the smaller tail wins unless the intervals T (1 -+ r) (r from the FP32
-    // error of x_m) come within 2.5e-15 (FP64 blend rounding and the 2^-53
+    // error of x_m) come within mrg (FP64 blend rounding and the 2^-53
     // quantisation of Pr); equal zero tails tie exactly and go by energy.
     const uint32_t ccls = __float_as_uint(sB[c1].y) & 0xFFFFFu;  // dnn << 8 | stage
+    // FP64 accuracy of a k-stage chain: ~2k + 2 roundings of <= 2^-53 plus the
+    // 2^-53 quantisation of each Pr (and erf's ulp): 1e-15 (2 + 2k) bounds the
+    // difference of two such accuracies with room to spare
+    const float mrg = 1e-15f * (2.0f + 2.0f * (float)max(1u, ccls & 0xFFu));
     bool ok1 = true;
     float ze1 = kInfF, ze2 = kInfF, bh = kInfF, bl = kInfF, lo2 = kInfF, nzlo = kInfF;
     int zc = -1, bc = -1;
@@ -1070,10 +1074,10 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
     int w;
     if (!ok1) return false;
     if (zc >= 0) {  // zero tails win; nonzero ones must be strictly worse
-      if (!(nzlo > 2.5e-15f) || !(ze2 > ze1 + ze1 * (4.0f * x.d_erel) + 1e-30f)) return false;
+      if (!(nzlo > mrg) || !(ze2 > ze1 + ze1 * (4.0f * x.d_erel) + 1e-30f)) return false;
       w = zc;
     } else {
-      if (bc < 0 || !(lo2 > bh + 2.5e-15f)) return false;
+      if (bc < 0 || !(lo2 > bh + mrg)) return false;
       w = bc;
     }
     if (!sure(w)) return false;
