@@ -157,10 +157,9 @@ __device__ __forceinline__ void fill_ratios(const DevTable& T, const Tile& tile,
 
 // The fused closed loop (simulator.run, simulator.py:461-507): one tile of W
 // lanes per stream, filter state in registers for the whole step range.
-// Register budget: 128 (16 warps / SM) for the general kernels; the
-// min-energy-only kernel gets ALERT_MINE_REGS (default 144: 14 warps / SM,
-// still one wave for 65,536 one-lane streams in 64-thread blocks) so its
-// per-step state stays out of local memory.
+// Register budget: 128 (16 warps / SM).  ALERT_MINE_REGS overrides it for
+// the min-energy-only kernel; 144 was measured slower (the register file is
+// split per SMSP, so 144 leaves 3 warps / scheduler and c2 needs two waves).
 #ifndef ALERT_MINE_REGS
 #define ALERT_MINE_REGS 128
 #endif

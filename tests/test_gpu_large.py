@@ -135,3 +135,36 @@ def test_c4_grid_tiles_agree_and_subset_vs_oracle(policy):
     rng = np.random.default_rng(3)
     base = "oracle" if policy == "oracle" else "alert"
     _subset_check(space, specs, packed, outs[32], rng.choice(len(ss), 6, replace=False), base, ss, sr)
+
+
+@pytest.fixture(scope="module")
+def c3():
+    space = A.preset_space()
+    ref = A.reference_latency(space)
+    specs = []
+    for dm in (0.6, 0.8, 1.2):
+        t = dm * ref
+        for pr in (0.95, 0.99):
+            specs.append(A.ConstraintSpec(mode=A.Mode.MAXIMIZE_ACCURACY, t_goal=t, e_goal=0.6 * 50.0 * t,
+                                          pr_threshold=pr, overhead_budget=0.01 * ref))
+    packed = preset_batch(4096, lengths=(334, 333, 333), seed0=4242, dtype=np.float32)
+    return space, specs, packed
+
+
+def test_c3_scale_subset_vs_oracle(c3):
+    """C3-style (max-accuracy + pr_th, anytime stages): the certified fast
+    max-accuracy scan and its near-tie fallbacks give the oracle's decisions."""
+    space, specs, packed = c3
+    res = A.run_batch(space, specs, packed, "alert", records="f32")
+    assert res.agg[:, abi.AGG_N].sum() == 4096 * 1000
+    rng = np.random.default_rng(11)
+    _subset_check(space, specs, packed, res, rng.choice(4096, 24, replace=False))
+
+
+def test_c3_scale_fast_scan_equals_full_scan(c3):
+    space, specs, packed = c3
+    a = A.run_batch(space, specs, packed, "alert", records="f32")
+    b = A.run_batch(space, specs, packed, "alert", records="f32", flags=abi.FLAG_NO_FAST)
+    np.testing.assert_array_equal(a.decoded()["cand"], b.decoded()["cand"])
+    np.testing.assert_array_equal(a.records["energy"], b.records["energy"])
+    np.testing.assert_array_equal(a.agg[:, :abi.AGG_LEVEL0], b.agg[:, :abi.AGG_LEVEL0])
