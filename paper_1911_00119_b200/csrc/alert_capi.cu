@@ -508,7 +508,35 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     unit_v[k] = make_int2(units[k].first, units[k].n);
     unit_lb[k] = (float)(2.0 - units[k].bound) - 1e-5f;
   }
+  // the same order flattened to one entry per cell for the W = 1 scan
+  // (fast_max_accuracy_flat): {cell, k | anytime << 3 | next group << 4, next
+  // unit, unit lb bits}, k = stage within the unit.  A group = the run of
+  // units of one DNN (equal bounds), re-ordered by latency ascending: a unit
+  // whose deadline-probability bound fails makes every later unit of the
+  // group fail too (1/t only falls), so the scan skips the group.
+  std::vector<int4> seq;
+  for (size_t g0 = 0; g0 < units.size();) {
+    const int dnn = tb->cand_dnn[order[units[g0].first]];
+    size_t g1 = g0 + 1;
+    while (g1 < units.size() && tb->cand_dnn[order[units[g1].first]] == dnn) ++g1;
+    std::vector<Unit> grp(units.begin() + g0, units.begin() + g1);
+    std::stable_sort(grp.begin(), grp.end(),
+                     [&](const Unit& a, const Unit& b) { return c64[a.first].t < c64[b.first].t; });
+    int cells = 0;
+    for (const Unit& u : grp) cells += u.n & 0xFFFF;
+    const int next_group = (int)seq.size() + cells;
+    for (const Unit& u : grp) {
+      const int m = u.n & 0xFFFF, next = (int)seq.size() + m;
+      const float lb = (float)(2.0 - u.bound) - 1e-5f;
+      int lbi;
+      memcpy(&lbi, &lb, 4);
+      for (int k = 0; k < m; ++k)
+        seq.push_back(make_int4(u.first + k, k | ((u.n >> 16) << 3) | (next_group << 4), next, lbi));
+    }
+    g0 = g1;
+  }
   size_t oUnit = place(sizeof(int2) * units.size()), oUlb = place(4 * units.size());
+  size_t oSeq = place(sizeof(int4) * seq.size());
   // comparison-scheme cells (policies.py:283-454): per power, the sys-only
   // DNN's cell and the first cell of the app-only DNN's column
   std::vector<int> sys_cells(P, -1), app_first(P, -1);
@@ -539,6 +567,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   if (!units.empty()) {
     memcpy(&h[oUnit], unit_v.data(), sizeof(int2) * units.size());
     memcpy(&h[oUlb], unit_lb.data(), 4 * units.size());
+    memcpy(&h[oSeq], seq.data(), sizeof(int4) * seq.size());
   }
   memcpy(&h[oApp], app_first.data(), 4 * P);
   e = cudaMemcpy(buf, h.data(), bytes, cudaMemcpyHostToDevice);
@@ -564,6 +593,8 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   T.units = units.empty() ? nullptr : reinterpret_cast<const int2*>(buf + oUnit);
   T.unit_lb = units.empty() ? nullptr : reinterpret_cast<const float*>(buf + oUlb);
   T.n_units = (int)units.size();
+  T.useq = seq.empty() ? nullptr : reinterpret_cast<const int4*>(buf + oSeq);
+  T.n_seq = (int)seq.size();
   T.app_first = app_stages > 0 ? reinterpret_cast<const int*>(buf + oApp) : nullptr;
   T.app_stages = app_stages;
   T.cap_max = (float)max_cap;
@@ -656,7 +687,7 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
       (P.fast_rows || (size_t)(tpb / W) * (size_t)(n_tdnn + 1) * 2 * sizeof(float) <= 16 * 1024))
     P.fast_smem = 1;  // alert_run computes the thresholds (zlo_kernel) and sets P.zlo
   // max-accuracy fast scan needs its sorted units in shared memory
-  if (P.fast_smem && any_max_accuracy && T.units && T.n_units <= 1024) P.units_smem = 1;
+  if (P.fast_smem && any_max_accuracy && T.units && T.n_units <= 1024 && T.n_seq <= 1024) P.units_smem = 1;
   P.c64_smem = T.n_cells <= kC64SmemMax;
   P.ratio_smem = T.n_powers <= kRatioSmemMax &&
                  (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;
@@ -674,7 +705,7 @@ static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const 
                P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
                (P.fast_smem && !P.fast_rows) ? T.n_trad / T.n_powers : 0,
                (P.fast_smem && !P.fast_rows) ? T.n_trad : 0, P.fast_smem && !P.fast_rows,
-               P.units_smem ? T.n_units : 0);
+               P.units_smem ? T.n_units : 0, P.units_smem ? T.n_seq : 0);
   return L.total;
 }
 

@@ -56,6 +56,8 @@ struct DevTable {
   const int2* units;      // {first cell, n cells | anytime << 16}
   const float* unit_lb;   // lower bound of any key of the unit: 2 - bound - 1e-5
   int n_units;
+  const int4* useq;       // units flattened per cell: {cell, k | anytime << 3 | next group << 4, next unit, lb bits}
+  int n_seq;              // == n_cells
   const int* sys_cells;   // [n_powers] or null
   const int* app_first;   // [n_powers] or null
   int app_stages;
@@ -180,6 +182,7 @@ struct StepCtx {
   bool any_window;      // ALERT_FLAG_ANY_WINDOW: two-pass window for anytime cells (A/B)
   const int2* su;       // max-accuracy fast scan: units / key lower bounds staged in shared memory
   const float* slb;
+  const int4* sq;       // T.useq staged in shared memory (or null: read through L1)
   float hs, hm;      // T_d = fma(z'_d, hs, hm)
   float Tpr;     // same for the pr_threshold z-bound (anytime cells)
 };
@@ -206,6 +209,7 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
   x.wst = nullptr;
   x.su = nullptr;
   x.slb = nullptr;
+  x.sq = nullptr;
   x.any_window = false;
   x.hs = x.hm = 0.f;
   x.Tpr = -kInfF;
@@ -1088,6 +1092,149 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
   }
 }
 
+// W = 1, up to 64 cells (the preset-sized tables): the same certified scan
+// with the bound-ordered units flattened to one loop over their cells
+// (T.useq), so every lane issues the same cell body each iteration instead of
+// a divergent chain loop nested in a unit loop; a unit whose first cell fails
+// the deadline-probability bound skips the rest of its DNN's group (units
+// sorted by latency).  Pass 1 runs on until the next unit's bound exceeds
+// both the running P2 and the running tie cut, and marks (64-bit mask over
+// sequence positions) every key within the running cut: the final cut is
+// never larger, so the near-tie pass (c') re-derives only the marked cells.
+template <bool HAS_PR>
+__device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const float4* __restrict__ sA,
+                                                       const float4* __restrict__ sB, const StepCtx& x,
+                                                       int kinds, Decision& d) {
+  const float mgH = -x.goal_f * kPenH;
+  const float elH = -x.e_lo * kPenH;
+  const int n_seq = T.n_seq;
+  // 32-bit shared addresses (no generic-to-shared conversion per cell)
+  const unsigned aq = (unsigned)__cvta_generic_to_shared(x.sq);
+  const unsigned aA = (unsigned)__cvta_generic_to_shared(sA);
+  auto seq_at = [&](int i) {
+    int4 v;
+    asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(aq + 16u * i));
+    return v;
+  };
+  auto cell_at = [&](int c) {
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(aA + 16u * c));
+    return v;
+  };
+  auto energy = [&](const float4& A) { return A.y * fmaxf(x.mu_e, fmaf(x.phig, A.x, x.ompmu)); };
+  auto penalty = [&](const float4& A, float E) {
+    const float pp = HAS_PR ? fmaf(mgH, A.x, x.Tpr) : -kInfF;
+    return fmaxf(fmaf(E, kPenH, elH), pp);
+  };
+  const float dcut = 2.0f * x.d_acc + 4e-6f;  // tie cut above P1: + truncation of both keys
+  Top2 t{kInfF, kInfF, -1};
+  unsigned long long marks = 0ull;
+  float acc = 0.0f;
+  for (int i = 0; i < n_seq; ++i) {
+    const int4 sq = seq_at(i);
+    const int k = sq.y & 7;
+    const float4 A = cell_at(sq.x);
+    const float pp = HAS_PR ? fmaf(mgH, A.x, x.Tpr) : -kInfF;
+    if (k == 0) {  // unit start: stop once no later unit can be P1, P2 or tied with P1
+      const float lb = __int_as_float(sq.w);
+      if (lb >= t.p2 && lb > t.p1 + dcut) break;
+      const int any = (sq.y >> 3) & 1;
+      if (!((kinds >> any) & 1) || (pp > 0.0f && (!any || T.any_mono))) {  // whole group out
+        i = (sq.y >> 4) - 1;
+        continue;
+      }
+      acc = A.w;
+    }
+    const float ph = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
+    const float E = energy(A);
+    const float pen = fmaxf(fmaf(E, kPenH, elH), pp);
+    acc = fmaf(ph, A.z, acc);
+    if (pen > 0.0f) {  // surely infeasible at L0 (see fast_max_accuracy)
+      if (T.any_mono && (pp > 0.0f || E > x.e_lo * (1.0f + x.d_erel))) i = sq.z - 1;  // rest of the chain
+      continue;
+    }
+    const float key = pack_key(fmaxf(2.0f - acc, pen), (unsigned)k);
+    const float before = t.p1;
+    t.push(key);
+    if (t.p1 != before) t.blk = sq.x - k;
+    if (key <= t.p1 + dcut) marks |= 1ull << i;
+  }
+  if (!(t.p1 < 2.0f) || t.blk < 0) return false;  // P1 must be a possible cell (no penalty)
+  const int c1 = t.blk + (int)(__float_as_uint(t.p1) & 7u);
+  if (c1 >= T.n_cells) return false;
+  auto sure = [&](int c) {
+    const float4 A = cell_at(c);
+    if (!(energy(A) <= x.e_hi)) return false;
+    if (!HAS_PR) return true;
+    return phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s) >= x.th_hi;
+  };
+  const float cut = t.p1 + dcut;
+  int w = c1;
+  if (!(t.p2 > cut)) {
+    // (c') near-ties within P1's class ordered by the deadline-miss tail, as
+    // in fast_max_accuracy: marked cells re-derived with their chain's tail
+    const uint32_t ccls = __float_as_uint(sB[c1].y) & 0xFFFFFu;
+    const float mrg = 1e-15f * (2.0f + 2.0f * (float)max(1u, ccls & 0xFFu));
+    bool ok1 = true;
+    float ze1 = kInfF, ze2 = kInfF, bh = kInfF, bl = kInfF, lo2 = kInfF, nzlo = kInfF;
+    int zc = -1, bc = -1;
+    while (marks) {
+      const int i = __ffsll((long long)marks) - 1;
+      marks &= marks - 1;
+      const int4 sq = seq_at(i);
+      const int k = sq.y & 7;
+      float a = 0.f, tail = 0.f, r = 0.f;
+      bool bad = false;
+      float4 A;
+      for (int m = sq.x - k; m <= sq.x; ++m) {  // the chain up to this cell, as pass 1 carried it
+        A = cell_at(m);
+        if (m == sq.x - k) a = A.w;
+        const float xz = fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s;
+        a = fmaf(phi32_x(xz), A.z, a);
+        if (!(xz >= kExactOneX)) {
+          bad |= !(xz >= 0.0f) || !(A.z >= 0.0f);
+          tail = fmaf(0.5f * erfc_rel(xz), A.z, tail);
+          const float dx = 4.0f * kEps * (fmaf(x.goal_f, A.x, fabsf(x.mu_f)) * x.inv_sig_s + fabsf(xz));
+          r = fmaxf(r, fmaf(2.0f * xz + 2.0f, dx, 1e-4f));
+        }
+      }
+      const float E = energy(A);
+      if (pack_key(fmaxf(2.0f - a, penalty(A, E)), (unsigned)k) > cut) continue;
+      const int c = sq.x;
+      if (bad || (__float_as_uint(sB[c].y) & 0xFFFFFu) != ccls) ok1 = false;
+      if (tail == 0.0f) {  // exact acc = a_k: energy decides among these
+        ze2 = fminf(ze2, fmaxf(ze1, E));
+        if (E < ze1) zc = c;
+        ze1 = fminf(ze1, E);
+      } else {
+        const float hi = tail * (1.0f + r), lo = tail * (1.0f - r);
+        nzlo = fminf(nzlo, lo);
+        if (hi < bh) {
+          lo2 = fminf(lo2, bl);
+          bh = hi;
+          bl = lo;
+          bc = c;
+        } else {
+          lo2 = fminf(lo2, lo);
+        }
+      }
+    }
+    if (!ok1) return false;
+    if (zc >= 0) {  // zero tails win; nonzero ones must be strictly worse
+      if (!(nzlo > mrg) || !(ze2 > ze1 + ze1 * (4.0f * x.d_erel) + 1e-30f)) return false;
+      w = zc;
+    } else {
+      if (bc < 0 || !(lo2 > bh + mrg)) return false;
+      w = bc;
+    }
+  }
+  if (!sure(w)) return false;
+  d.cell = w;
+  d.level = 0;
+  d.refined = false;
+  return true;
+}
+
 // Re-rank pass from the stored FP32 objectives (no re-scan): the same
 // cell-to-lane assignment as cell_pass, so each lane reads what it wrote.
 template <int MODE, bool HAS_PR, class Tile>
@@ -1231,7 +1378,9 @@ __device__ __forceinline__ Decision alert_decide_t(const DevTable& T, const floa
   if (MODE == ALERT_MODE_MAX_ACCURACY && x.fast && !x.fp64_all && T.units) {
     const unsigned am = __activemask();
     Decision d{-1, 0, false};
-    const bool ok = fast_max_accuracy<HAS_PR>(T, sA, sB, tile, x, kinds, d);
+    const bool ok = (Tile::num_threads() == 1 && x.sq && T.n_seq <= 64)
+                        ? fast_max_accuracy_flat<HAS_PR>(T, sA, sB, x, kinds, d)
+                        : fast_max_accuracy<HAS_PR>(T, sA, sB, tile, x, kinds, d);
     __syncwarp(am);
     if (ok) return d;
     tried = true;

@@ -60,7 +60,7 @@ struct SmemLayout {
   __host__ __device__ static int pad_rows(int W) { return 8 * W + 8; }
   __host__ __device__ SmemLayout(int n_cells, int n_cols, int n_spec, int n_c64, int n_tiles, int n_ratio,
                                  size_t agg_bytes, int n_sv, int W, int n_fz = 0, int n_ff = 0,
-                                 bool flat = false, int n_un = 0) {
+                                 bool flat = false, int n_un = 0, int n_sq = 0) {
     B = sizeof(float4) * (size_t)(n_cells + pad_rows(W));
     col = B + sizeof(float4) * (size_t)n_cells;
     spec = up16(col + sizeof(int2) * (size_t)(n_cols + pad_rows(W)));
@@ -71,8 +71,8 @@ struct SmemLayout {
     fz = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);  // 2 x [n_fz][n_tiles]: Z, T
     ff = up16(fz + 2 * sizeof(float) * (size_t)n_tiles * (size_t)n_fz);  // fast-scan traditional cells
     wst = up16(ff + (flat ? sizeof(float4) * (size_t)(n_ff + pad_rows(W)) : 0));
-    un = up16(wst + (flat ? sizeof(unsigned) * (size_t)(n_cells / 32 + 2) : 0));  // units, then lbs
-    cold = up16(un + (sizeof(int2) + sizeof(float)) * (size_t)n_un);
+    un = up16(wst + (flat ? sizeof(unsigned) * (size_t)(n_cells / 32 + 2) : 0));  // sequence, units, lbs
+    cold = up16(un + sizeof(int4) * (size_t)n_sq + (sizeof(int2) + sizeof(float)) * (size_t)n_un);
     slot = up16(cold + sizeof(ColdState) * (size_t)n_tiles * (size_t)W);
     total = up16(slot + 16 * (size_t)n_tiles * (size_t)W);  // two 8-byte trace slots per thread
   }
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   const SmemLayout L(T.n_cells, T.n_any_cols, n_tiles, P.c64_smem ? T.n_cells : 0, n_tiles,
                      P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
                      (P.zlo && !P.fast_rows) ? n_tdnn : 0, (P.zlo && !P.fast_rows) ? T.n_trad : 0,
-                     P.zlo && !P.fast_rows, P.units_smem ? T.n_units : 0);
+                     P.zlo && !P.fast_rows, P.units_smem ? T.n_units : 0, P.units_smem ? T.n_seq : 0);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
   float4* sB = reinterpret_cast<float4*>(base + L.B);
@@ -195,13 +195,16 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       sF[i] = make_float4(in ? T.cellA[i].x : 0.f, in ? T.cellA[i].y : 0.f, __int_as_float(off),
                           __int_as_float((i / W) & 7));
     }
-  int2* sUn = reinterpret_cast<int2*>(base + L.un);
+  int4* sSq = reinterpret_cast<int4*>(base + L.un);
+  int2* sUn = reinterpret_cast<int2*>(sSq + (P.units_smem ? T.n_seq : 0));
   float* sLb = reinterpret_cast<float*>(sUn + (P.units_smem ? T.n_units : 0));
-  if (P.units_smem)
+  if (P.units_smem) {
     for (int i = threadIdx.x; i < T.n_units; i += blockDim.x) {
       sUn[i] = T.units[i];
       sLb[i] = T.unit_lb[i];
     }
+    for (int i = threadIdx.x; i < T.n_seq; i += blockDim.x) sSq[i] = T.useq[i];
+  }
   unsigned* sWst = reinterpret_cast<unsigned*>(base + L.wst);
   if (P.zlo && !P.fast_rows)  // column-start bits of the anytime cells, per 32-cell window
     for (int w = threadIdx.x; w * 32 < T.n_cells - T.n_trad; w += blockDim.x) {
@@ -363,6 +366,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
         if (P.units_smem) {
           x.su = sUn;
           x.slb = sLb;
+          x.sq = sSq;
         }
         float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
         fast_prep(x, tile, fzZ, fzZ + (size_t)n_tiles * n_tdnn, n_tiles, fast_me ? n_tdnn : 0, zpr,
