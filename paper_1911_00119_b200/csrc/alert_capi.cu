@@ -509,34 +509,41 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     unit_lb[k] = (float)(2.0 - units[k].bound) - 1e-5f;
   }
   // the same order flattened to one entry per cell for the W = 1 scan
-  // (fast_max_accuracy_flat): {cell, k | anytime << 3 | next group << 4, next
-  // unit, unit lb bits}, k = stage within the unit.  A group = the run of
-  // units of one DNN (equal bounds), re-ordered by latency ascending: a unit
-  // whose deadline-probability bound fails makes every later unit of the
-  // group fail too (1/t only falls), so the scan skips the group.
-  std::vector<int4> seq;
-  for (size_t g0 = 0; g0 < units.size();) {
-    const int dnn = tb->cand_dnn[order[units[g0].first]];
-    size_t g1 = g0 + 1;
-    while (g1 < units.size() && tb->cand_dnn[order[units[g1].first]] == dnn) ++g1;
-    std::vector<Unit> grp(units.begin() + g0, units.begin() + g1);
-    std::stable_sort(grp.begin(), grp.end(),
-                     [&](const Unit& a, const Unit& b) { return c64[a.first].t < c64[b.first].t; });
-    int cells = 0;
-    for (const Unit& u : grp) cells += u.n & 0xFFFF;
-    const int next_group = (int)seq.size() + cells;
-    for (const Unit& u : grp) {
-      const int m = u.n & 0xFFFF, next = (int)seq.size() + m;
-      const float lb = (float)(2.0 - u.bound) - 1e-5f;
-      int lbi;
-      memcpy(&lbi, &lb, 4);
-      for (int k = 0; k < m; ++k)
-        seq.push_back(make_int4(u.first + k, k | ((u.n >> 16) << 3) | (next_group << 4), next, lbi));
+  // (fast_max_accuracy_flat, tables of <= 64 cells): the cell's cellA row and
+  // {cell | k << 7 | anytime << 10 | next group << 11 | next unit << 18, unit
+  // lb bits}, k = stage within the unit.  A group = the run of units of one
+  // DNN (equal bounds), re-ordered by latency ascending: a unit whose
+  // deadline-probability bound fails makes every later unit of the group fail
+  // too (1/t only falls), so the scan skips the group.
+  std::vector<float4> seqA;
+  std::vector<int2> seqM;
+  if (n <= 64) {
+    for (size_t g0 = 0; g0 < units.size();) {
+      const int dnn = tb->cand_dnn[order[units[g0].first]];
+      size_t g1 = g0 + 1;
+      while (g1 < units.size() && tb->cand_dnn[order[units[g1].first]] == dnn) ++g1;
+      std::vector<Unit> grp(units.begin() + g0, units.begin() + g1);
+      std::stable_sort(grp.begin(), grp.end(),
+                       [&](const Unit& a, const Unit& b) { return c64[a.first].t < c64[b.first].t; });
+      int cells = 0;
+      for (const Unit& u : grp) cells += u.n & 0xFFFF;
+      const int next_group = (int)seqM.size() + cells;
+      for (const Unit& u : grp) {
+        const int m = u.n & 0xFFFF, next = (int)seqM.size() + m;
+        const float lb = (float)(2.0 - u.bound) - 1e-5f;
+        int lbi;
+        memcpy(&lbi, &lb, 4);
+        for (int k = 0; k < m; ++k) {
+          seqA.push_back(A[u.first + k]);
+          seqM.push_back(make_int2((u.first + k) | (k << 7) | ((u.n >> 16) << 10) | (next_group << 11) | (next << 18),
+                                   lbi));
+        }
+      }
+      g0 = g1;
     }
-    g0 = g1;
   }
   size_t oUnit = place(sizeof(int2) * units.size()), oUlb = place(4 * units.size());
-  size_t oSeq = place(sizeof(int4) * seq.size());
+  size_t oSeqA = place(sizeof(float4) * seqA.size()), oSeqM = place(sizeof(int2) * seqM.size());
   // comparison-scheme cells (policies.py:283-454): per power, the sys-only
   // DNN's cell and the first cell of the app-only DNN's column
   std::vector<int> sys_cells(P, -1), app_first(P, -1);
@@ -567,7 +574,10 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   if (!units.empty()) {
     memcpy(&h[oUnit], unit_v.data(), sizeof(int2) * units.size());
     memcpy(&h[oUlb], unit_lb.data(), 4 * units.size());
-    memcpy(&h[oSeq], seq.data(), sizeof(int4) * seq.size());
+  }
+  if (!seqM.empty()) {
+    memcpy(&h[oSeqA], seqA.data(), sizeof(float4) * seqA.size());
+    memcpy(&h[oSeqM], seqM.data(), sizeof(int2) * seqM.size());
   }
   memcpy(&h[oApp], app_first.data(), 4 * P);
   e = cudaMemcpy(buf, h.data(), bytes, cudaMemcpyHostToDevice);
@@ -593,8 +603,9 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   T.units = units.empty() ? nullptr : reinterpret_cast<const int2*>(buf + oUnit);
   T.unit_lb = units.empty() ? nullptr : reinterpret_cast<const float*>(buf + oUlb);
   T.n_units = (int)units.size();
-  T.useq = seq.empty() ? nullptr : reinterpret_cast<const int4*>(buf + oSeq);
-  T.n_seq = (int)seq.size();
+  T.useqA = seqM.empty() ? nullptr : reinterpret_cast<const float4*>(buf + oSeqA);
+  T.useqM = seqM.empty() ? nullptr : reinterpret_cast<const int2*>(buf + oSeqM);
+  T.n_seq = (int)seqM.size();
   T.app_first = app_stages > 0 ? reinterpret_cast<const int*>(buf + oApp) : nullptr;
   T.app_stages = app_stages;
   T.cap_max = (float)max_cap;
@@ -687,7 +698,7 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
       (P.fast_rows || (size_t)(tpb / W) * (size_t)(n_tdnn + 1) * 2 * sizeof(float) <= 16 * 1024))
     P.fast_smem = 1;  // alert_run computes the thresholds (zlo_kernel) and sets P.zlo
   // max-accuracy fast scan needs its sorted units in shared memory
-  if (P.fast_smem && any_max_accuracy && T.units && T.n_units <= 1024 && T.n_seq <= 1024) P.units_smem = 1;
+  if (P.fast_smem && any_max_accuracy && T.units && T.n_units <= 1024) P.units_smem = 1;
   P.c64_smem = T.n_cells <= kC64SmemMax;
   P.ratio_smem = T.n_powers <= kRatioSmemMax &&
                  (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;

@@ -56,8 +56,11 @@ struct DevTable {
   const int2* units;      // {first cell, n cells | anytime << 16}
   const float* unit_lb;   // lower bound of any key of the unit: 2 - bound - 1e-5
   int n_units;
-  const int4* useq;       // units flattened per cell: {cell, k | anytime << 3 | next group << 4, next unit, lb bits}
-  int n_seq;              // == n_cells
+  // units flattened per cell (tables of <= 64 cells, else n_seq = 0): cellA
+  // rows and {cell | k << 7 | anytime << 10 | next group << 11 | next unit << 18, lb}
+  const float4* useqA;
+  const int2* useqM;
+  int n_seq;
   const int* sys_cells;   // [n_powers] or null
   const int* app_first;   // [n_powers] or null
   int app_stages;
@@ -182,7 +185,8 @@ struct StepCtx {
   bool any_window;      // ALERT_FLAG_ANY_WINDOW: two-pass window for anytime cells (A/B)
   const int2* su;       // max-accuracy fast scan: units / key lower bounds staged in shared memory
   const float* slb;
-  const int4* sq;       // T.useq staged in shared memory (or null: read through L1)
+  const float4* sqA;    // T.useqA / T.useqM staged in shared memory (or null)
+  const int2* sqM;
   float hs, hm;      // T_d = fma(z'_d, hs, hm)
   float Tpr;     // same for the pr_threshold z-bound (anytime cells)
 };
@@ -209,7 +213,8 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
   x.wst = nullptr;
   x.su = nullptr;
   x.slb = nullptr;
-  x.sq = nullptr;
+  x.sqA = nullptr;
+  x.sqM = nullptr;
   x.any_window = false;
   x.hs = x.hm = 0.f;
   x.Tpr = -kInfF;
@@ -1108,19 +1113,23 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
   const float mgH = -x.goal_f * kPenH;
   const float elH = -x.e_lo * kPenH;
   const int n_seq = T.n_seq;
-  // 32-bit shared addresses (no generic-to-shared conversion per cell)
-  const unsigned aq = (unsigned)__cvta_generic_to_shared(x.sq);
+  const bool mono = T.any_mono;
+  // 32-bit shared addresses (no generic-to-shared conversion per cell); the
+  // row and the metadata of an entry are independent loads
+  const unsigned aqa = (unsigned)__cvta_generic_to_shared(x.sqA);
+  const unsigned aqm = (unsigned)__cvta_generic_to_shared(x.sqM);
   const unsigned aA = (unsigned)__cvta_generic_to_shared(sA);
-  auto seq_at = [&](int i) {
-    int4 v;
-    asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(aq + 16u * i));
-    return v;
-  };
-  auto cell_at = [&](int c) {
+  auto f4 = [](unsigned a) {
     float4 v;
-    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(aA + 16u * c));
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
     return v;
   };
+  auto meta_at = [&](int i) {
+    int2 v;
+    asm("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(aqm + 8u * i));
+    return v;
+  };
+  auto cell_at = [&](int c) { return f4(aA + 16u * c); };
   auto energy = [&](const float4& A) { return A.y * fmaxf(x.mu_e, fmaf(x.phig, A.x, x.ompmu)); };
   auto penalty = [&](const float4& A, float E) {
     const float pp = HAS_PR ? fmaf(mgH, A.x, x.Tpr) : -kInfF;
@@ -1131,33 +1140,36 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
   unsigned long long marks = 0ull;
   float acc = 0.0f;
   for (int i = 0; i < n_seq; ++i) {
-    const int4 sq = seq_at(i);
-    const int k = sq.y & 7;
-    const float4 A = cell_at(sq.x);
+    const float4 A = f4(aqa + 16u * i);
+    const int2 M = meta_at(i);
+    const unsigned long long bit = 1ull << i;
+    const int k = (M.x >> 7) & 7;
     const float pp = HAS_PR ? fmaf(mgH, A.x, x.Tpr) : -kInfF;
-    if (k == 0) {  // unit start: stop once no later unit can be P1, P2 or tied with P1
-      const float lb = __int_as_float(sq.w);
-      if (lb >= t.p2 && lb > t.p1 + dcut) break;
-      const int any = (sq.y >> 3) & 1;
-      if (!((kinds >> any) & 1) || (pp > 0.0f && (!any || T.any_mono))) {  // whole group out
-        i = (sq.y >> 4) - 1;
-        continue;
-      }
-      acc = A.w;
-    }
+    // unit start: stop once no later unit can be P1, P2 or tied with P1
+    const bool start = k == 0;
+    const float lb = __int_as_float(M.y);
+    if (start && lb >= t.p2 && lb > t.p1 + dcut) break;
+    // the rest is predicated (no divergent paths inside the loop): a skipped
+    // group / chain costs one cell body and moves i
+    const int any = (M.x >> 10) & 1;
+    const bool skip = start && (!((kinds >> any) & 1) || (pp > 0.0f && (!any || mono)));  // group out
+    if (start) acc = A.w;
     const float ph = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
     const float E = energy(A);
     const float pen = fmaxf(fmaf(E, kPenH, elH), pp);
     acc = fmaf(ph, A.z, acc);
-    if (pen > 0.0f) {  // surely infeasible at L0 (see fast_max_accuracy)
-      if (T.any_mono && (pp > 0.0f || E > x.e_lo * (1.0f + x.d_erel))) i = sq.z - 1;  // rest of the chain
-      continue;
-    }
-    const float key = pack_key(fmaxf(2.0f - acc, pen), (unsigned)k);
+    // surely infeasible at L0 (see fast_max_accuracy): no key; with monotone
+    // stage latencies the rest of the chain is out too
+    const bool out = skip || pen > 0.0f;
+    int nxt = i;
+    if (out && mono && (pp > 0.0f || E > x.e_lo * (1.0f + x.d_erel))) nxt = ((M.x >> 18) & 127) - 1;
+    if (skip) nxt = ((M.x >> 11) & 127) - 1;
+    i = nxt;
+    const float key = out ? kInfF : pack_key(fmaxf(2.0f - acc, pen), (unsigned)k);
     const float before = t.p1;
     t.push(key);
-    if (t.p1 != before) t.blk = sq.x - k;
-    if (key <= t.p1 + dcut) marks |= 1ull << i;
+    if (t.p1 != before) t.blk = (M.x & 127) - k;
+    if (key <= fminf(t.p1 + dcut, 3.0f)) marks |= bit;
   }
   if (!(t.p1 < 2.0f) || t.blk < 0) return false;  // P1 must be a possible cell (no penalty)
   const int c1 = t.blk + (int)(__float_as_uint(t.p1) & 7u);
@@ -1181,14 +1193,14 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
     while (marks) {
       const int i = __ffsll((long long)marks) - 1;
       marks &= marks - 1;
-      const int4 sq = seq_at(i);
-      const int k = sq.y & 7;
+      const int2 M = meta_at(i);
+      const int k = (M.x >> 7) & 7, c = M.x & 127;
       float a = 0.f, tail = 0.f, r = 0.f;
       bool bad = false;
       float4 A;
-      for (int m = sq.x - k; m <= sq.x; ++m) {  // the chain up to this cell, as pass 1 carried it
+      for (int m = c - k; m <= c; ++m) {  // the chain up to this cell, as pass 1 carried it
         A = cell_at(m);
-        if (m == sq.x - k) a = A.w;
+        if (m == c - k) a = A.w;
         const float xz = fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s;
         a = fmaf(phi32_x(xz), A.z, a);
         if (!(xz >= kExactOneX)) {
@@ -1200,7 +1212,6 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
       }
       const float E = energy(A);
       if (pack_key(fmaxf(2.0f - a, penalty(A, E)), (unsigned)k) > cut) continue;
-      const int c = sq.x;
       if (bad || (__float_as_uint(sB[c].y) & 0xFFFFFu) != ccls) ok1 = false;
       if (tail == 0.0f) {  // exact acc = a_k: energy decides among these
         ze2 = fminf(ze2, fmaxf(ze1, E));
@@ -1378,7 +1389,7 @@ __device__ __forceinline__ Decision alert_decide_t(const DevTable& T, const floa
   if (MODE == ALERT_MODE_MAX_ACCURACY && x.fast && !x.fp64_all && T.units) {
     const unsigned am = __activemask();
     Decision d{-1, 0, false};
-    const bool ok = (Tile::num_threads() == 1 && x.sq && T.n_seq <= 64)
+    const bool ok = (Tile::num_threads() == 1 && x.sqA)
                         ? fast_max_accuracy_flat<HAS_PR>(T, sA, sB, x, kinds, d)
                         : fast_max_accuracy<HAS_PR>(T, sA, sB, tile, x, kinds, d);
     __syncwarp(am);

@@ -72,7 +72,7 @@ struct SmemLayout {
     ff = up16(fz + 2 * sizeof(float) * (size_t)n_tiles * (size_t)n_fz);  // fast-scan traditional cells
     wst = up16(ff + (flat ? sizeof(float4) * (size_t)(n_ff + pad_rows(W)) : 0));
     un = up16(wst + (flat ? sizeof(unsigned) * (size_t)(n_cells / 32 + 2) : 0));  // sequence, units, lbs
-    cold = up16(un + sizeof(int4) * (size_t)n_sq + (sizeof(int2) + sizeof(float)) * (size_t)n_un);
+    cold = up16(un + (sizeof(float4) + sizeof(int2)) * (size_t)n_sq + (sizeof(int2) + sizeof(float)) * (size_t)n_un);
     slot = up16(cold + sizeof(ColdState) * (size_t)n_tiles * (size_t)W);
     total = up16(slot + 16 * (size_t)n_tiles * (size_t)W);  // two 8-byte trace slots per thread
   }
@@ -195,15 +195,19 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       sF[i] = make_float4(in ? T.cellA[i].x : 0.f, in ? T.cellA[i].y : 0.f, __int_as_float(off),
                           __int_as_float((i / W) & 7));
     }
-  int4* sSq = reinterpret_cast<int4*>(base + L.un);
-  int2* sUn = reinterpret_cast<int2*>(sSq + (P.units_smem ? T.n_seq : 0));
+  float4* sQA = reinterpret_cast<float4*>(base + L.un);
+  int2* sQM = reinterpret_cast<int2*>(sQA + (P.units_smem ? T.n_seq : 0));
+  int2* sUn = sQM + (P.units_smem ? T.n_seq : 0);
   float* sLb = reinterpret_cast<float*>(sUn + (P.units_smem ? T.n_units : 0));
   if (P.units_smem) {
     for (int i = threadIdx.x; i < T.n_units; i += blockDim.x) {
       sUn[i] = T.units[i];
       sLb[i] = T.unit_lb[i];
     }
-    for (int i = threadIdx.x; i < T.n_seq; i += blockDim.x) sSq[i] = T.useq[i];
+    for (int i = threadIdx.x; i < T.n_seq; i += blockDim.x) {
+      sQA[i] = T.useqA[i];
+      sQM[i] = T.useqM[i];
+    }
   }
   unsigned* sWst = reinterpret_cast<unsigned*>(base + L.wst);
   if (P.zlo && !P.fast_rows)  // column-start bits of the anytime cells, per 32-cell window
@@ -366,7 +370,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
         if (P.units_smem) {
           x.su = sUn;
           x.slb = sLb;
-          x.sq = sSq;
+          if (T.n_seq) {
+            x.sqA = sQA;
+            x.sqM = sQM;
+          }
         }
         float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
         fast_prep(x, tile, fzZ, fzZ + (size_t)n_tiles * n_tdnn, n_tiles, fast_me ? n_tdnn : 0, zpr,
