@@ -106,7 +106,8 @@ def build_workload(cfg: str, n_streams: int, n_steps: int, rank: int, world: int
     parts = []
     rng = np.random.default_rng(1000)
     orders = [tuple(rng.permutation(3)) for _ in range(n_traces)]
-    cuts = [np.sort(rng.integers(100, n_steps - 100, 2)) for _ in range(n_traces)]
+    m = min(100, n_steps // 4)  # phase cuts at least m steps from either end (100 at full size)
+    cuts = [np.sort(rng.integers(m, n_steps - m, 2)) for _ in range(n_traces)]
     for t in range(n_traces):
         a, b = cuts[t]
         lengths = (int(a), int(b - a), int(n_steps - b))

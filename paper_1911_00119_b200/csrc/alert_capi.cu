@@ -542,6 +542,23 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
       g0 = g1;
     }
   }
+  // min-energy row mode: traditional DNN rows {dnn bits, smallest cap * t,
+  // largest 1/t, 0} by their smallest cap * t, ascending
+  std::vector<float4> trows;
+  if (P > 0 && !trad_cells.empty()) {
+    for (int dn = 0; dn < (int)trad_cells.size() / P; ++dn) {
+      float m = A[(size_t)dn * P].y, ax = A[(size_t)dn * P].x;
+      for (int j = 1; j < P; ++j) {
+        m = std::min(m, A[(size_t)dn * P + j].y);
+        ax = std::max(ax, A[(size_t)dn * P + j].x);
+      }
+      float dnf;
+      memcpy(&dnf, &dn, 4);
+      trows.push_back(make_float4(dnf, m, ax, 0.0f));
+    }
+    std::stable_sort(trows.begin(), trows.end(), [](const float4& a, const float4& b) { return a.y < b.y; });
+  }
+  size_t oTrows = place(sizeof(float4) * trows.size());
   size_t oUnit = place(sizeof(int2) * units.size()), oUlb = place(4 * units.size());
   size_t oSeqA = place(sizeof(float4) * seqA.size()), oSeqM = place(sizeof(int2) * seqM.size());
   // comparison-scheme cells (policies.py:283-454): per power, the sys-only
@@ -575,6 +592,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     memcpy(&h[oUnit], unit_v.data(), sizeof(int2) * units.size());
     memcpy(&h[oUlb], unit_lb.data(), 4 * units.size());
   }
+  if (!trows.empty()) memcpy(&h[oTrows], trows.data(), sizeof(float4) * trows.size());
   if (!seqM.empty()) {
     memcpy(&h[oSeqA], seqA.data(), sizeof(float4) * seqA.size());
     memcpy(&h[oSeqM], seqM.data(), sizeof(int2) * seqM.size());
@@ -606,9 +624,12 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   T.useqA = seqM.empty() ? nullptr : reinterpret_cast<const float4*>(buf + oSeqA);
   T.useqM = seqM.empty() ? nullptr : reinterpret_cast<const int2*>(buf + oSeqM);
   T.n_seq = (int)seqM.size();
+  T.trad_rows = trows.empty() ? nullptr : reinterpret_cast<const float4*>(buf + oTrows);
   T.app_first = app_stages > 0 ? reinterpret_cast<const int*>(buf + oApp) : nullptr;
   T.app_stages = app_stages;
   T.cap_max = (float)max_cap;
+  T.cap_min = (float)d->power_cap[0];
+  for (int j = 1; j < P; ++j) T.cap_min = std::min(T.cap_min, (float)d->power_cap[j]);
   T.any_mono = 1;  // fast scan's anytime skip (fast_min_energy): stage latencies non-decreasing
   for (const int2& cd : cols)
     for (int k = 1; k < cd.y; ++k)

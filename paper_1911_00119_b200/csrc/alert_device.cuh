@@ -61,6 +61,9 @@ struct DevTable {
   const float4* useqA;
   const int2* useqM;
   int n_seq;
+  const float4* trad_rows;  // min-energy row mode: {dnn bits, min cap * t, max 1/t, 0}, min cap * t ascending
+  float cap_min;            // smallest cap (FP32)
+
   const int* sys_cells;   // [n_powers] or null
   const int* app_first;   // [n_powers] or null
   int app_stages;
@@ -662,12 +665,34 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
     // row mode (large tables): DNN-major, lanes split the powers of a row in
     // chunks of 8 (masked at the row end); T_d from the spec's z' (L1), the
     // next DNN's z' in flight while the current row is scanned
+    // Rows go by their smallest cap * t (m_r), ascending.  Every key of a
+    // row is >= cap t max(mu_e, phig / t + ompmu) >= max(mu_e m_r, phig
+    // cap_min + ompmu m_r) (phig, ompmu >= 0; the penalty only raises a key),
+    // a bound increasing with m_r: once it (scaled by 1 - 4e-6 for the FP32
+    // rounding and the packed key's truncation) reaches the lane's P2, no
+    // cell of this or any later row can enter (P1, P2) and the scan stops.
     const int P = T.n_powers;
     const int n_tdnn = T.n_trad / P;
-    float zn = __ldg(x.zrow);
-    for (int dn = 0; dn < n_tdnn; ++dn) {
+    const float mu_es = x.mu_e * (1.0f - 4e-6f);
+    const bool lin = x.ompmu >= 0.0f && x.phig >= 0.0f;  // else the mu_e bound alone
+    const float om_s = lin ? x.ompmu * (1.0f - 4e-6f) : 0.0f;
+    const float ph_s = lin ? x.phig * T.cap_min * (1.0f - 4e-6f) : 0.0f;
+    float4 rw = n_tdnn > 0 ? __ldg(T.trad_rows) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float zn = n_tdnn > 0 ? __ldg(x.zrow + __float_as_int(rw.x)) : 0.f;
+    for (int r = 0; r < n_tdnn; ++r) {
+      if (fmaxf(rw.y * mu_es, fmaf(om_s, rw.y, ph_s)) >= t.p2) break;
+      const int dn = __float_as_int(rw.x);
       const float Td = fmaf(zn, x.hs, x.hm);
-      if (dn + 1 < n_tdnn) zn = __ldg(x.zrow + dn + 1);
+      // a row whose fastest cell already carries the deadline / accuracy
+      // penalty (fma monotone in 1/t: so does every cell) is surely
+      // infeasible at level 0 throughout: it can neither be a certified P1
+      // nor undercut one, so it is not scanned
+      const bool dead = fmaf(mgH, rw.z, Td) > 0.0f;
+      if (r + 1 < n_tdnn) {
+        rw = __ldg(T.trad_rows + r + 1);
+        zn = __ldg(x.zrow + __float_as_int(rw.x));
+      }
+      if (dead) continue;
       const float4* row = sA + dn * P;  // padded table: reads past the row are masked
       for (int p0 = lane; p0 < P; p0 += 8 * W) {
         const float s1 = t.p1;
