@@ -12,7 +12,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 for cfg in c2 c3 c4; do
   case $cfg in
     c2) extra="--trace-steps 1000";;
-    c3) extra="--config c3 --streams 262144 --trace-steps 200";;
+    c3) extra="--config c3 --streams 1048576 --trace-steps 30";;
     c4) extra="--config c4 --streams 65536 --trace-steps 300";;
   esac
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:run_kernel -c 1 -f -o /tmp/prof_$cfg python bench.py --steps 1 --warmup 0 $extra --no-cpu --no-e2e > gpurun_out/ncu_$cfg.log 2>&1
