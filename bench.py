@@ -443,7 +443,7 @@ def main():
             "data": "synthetic: reference preset contention traces realized with numpy (seed 42+stream)",
             "config": {"workload": args.config, "desc": desc, "streams_per_rank": S, "steps_per_stream": N,
                        "candidates": C, "policy": policy, "records": args.records,
-                       "lanes_per_stream": lanes or (1 if C <= 256 else 4),
+                       "lanes_per_stream": lanes or (1 if C <= 256 else 8),
                        "threads_per_block": tpb if args.tpb else "auto (64; 256 when the staged table > 40 KB)",
                        "l2": "inputs larger than L2" if 4 * S * N > 126e6 else "inputs fit L2",
                        "parallelism": f"streams sharded, {world} rank(s)"},

@@ -743,9 +743,12 @@ static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const 
 
 static int pick_lanes(const AlertContext* ctx, const AlertTable* tb) {
   if (ctx->lanes) return ctx->lanes;
-  // measured on B200 (profiles/): one lane per stream for small tables (no
-  // redundant per-step work), 4-lane tiles for the 2,144-candidate table
-  return tb->n_cand <= 256 ? 1 : 4;
+  // measured on B200 (profiles/r01b_lanes_c4.txt): one lane per stream for
+  // small tables (no redundant per-step work), 8-lane tiles for the
+  // 2,144-candidate table (c4: 2 / 4 / 8 / 16 / 32 lanes -> 2.37 / 2.03 /
+  // 2.55 / 2.05 / 1.20 e8 decisions/s; 4 streams per warp bound the wait
+  // for the slowest stream's row scan)
+  return tb->n_cand <= 256 ? 1 : 8;
 }
 
 // Upload host specs to stream-ordered device memory (freed after the launch).
