@@ -114,12 +114,8 @@ __device__ inline double zlo_of_prob(double p) {
   double z = p >= 1.0 ? 7.5 : fmin(normcdfinv(p), 7.5);
   return z - 1e-9 * (1.0 + fabs(z));
 }
-__global__ void zlo_kernel(const SpecDev* specs, int n_specs, const Cell64* c64, int P, int n_tdnn, float* out) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int stride = n_tdnn + 1;
-  if (i >= (long long)n_specs * stride) return;
-  const int s = (int)(i / stride), d = (int)(i % stride);
-  const SpecDev& sp = specs[s];
+// z' of spec s, traditional DNN d (d == n_tdnn: the pr_threshold bound)
+__device__ float zlo_value(const SpecDev& sp, const Cell64* c64, int P, int n_tdnn, int d) {
   const double zpr = sp.has_pr ? zlo_of_prob(sp.pr_th - 1e-15) : -kInf;
   double z;
   if (d == n_tdnn) {
@@ -138,7 +134,21 @@ __global__ void zlo_kernel(const SpecDev* specs, int n_specs, const Cell64* c64,
     z = fmax(z, zpr);
   }
   const float zf = z == kInf ? 1e10f : (float)z;
-  out[i] = fmaf(-20.0f * kEps, fabsf(zf), zf);
+  return fmaf(-20.0f * kEps, fabsf(zf), zf);
+}
+// out: [n_specs][n_tdnn + 1] by DNN, then (rows != null, row mode)
+// [n_specs][n_tdnn] in the scan's row order (rows[r].x = DNN bits)
+__global__ void zlo_kernel(const SpecDev* specs, int n_specs, const Cell64* c64, int P, int n_tdnn,
+                           const float4* rows, float* out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int stride = n_tdnn + 1;
+  const long long n1 = (long long)n_specs * stride;
+  if (i < n1) {
+    out[i] = zlo_value(specs[i / stride], c64, P, n_tdnn, (int)(i % stride));
+  } else if (rows && n_tdnn > 0 && i < n1 + (long long)n_specs * n_tdnn) {
+    const long long j = i - n1;
+    out[i] = zlo_value(specs[j / n_tdnn], c64, P, n_tdnn, __float_as_int(rows[j % n_tdnn].x));
+  }
 }
 
 
@@ -973,10 +983,11 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   float* dzlo = nullptr;
   if (P.fast_smem) {  // fast scan staged by run_staging: compute the thresholds on the stream
     const int n_tdnn = tb->dev.n_trad / tb->dev.n_powers;
-    const long long nz = (long long)n_specs * (n_tdnn + 1);
+    const float4* rows = P.fast_rows ? tb->dev.trad_rows : nullptr;
+    const long long nz = (long long)n_specs * (n_tdnn + 1) + (rows ? (long long)n_specs * n_tdnn : 0);
     CUDA_TRY(cudaMallocAsync((void**)&dzlo, sizeof(float) * nz, s));
     zlo_kernel<<<(unsigned)((nz + 127) / 128), 128, 0, s>>>(dspecs, n_specs, tb->dev.c64, tb->dev.n_powers, n_tdnn,
-                                                          dzlo);
+                                                          rows, dzlo);
     CUDA_TRY(cudaGetLastError());
     ctx->launches++;
     P.zlo = dzlo;

@@ -183,7 +183,7 @@ struct StepCtx {
   const float* tT;
   int tS;
   const float4* sF;  // traditional cells {1/t, cap t, byte offset of the DNN's threshold in tT, 0}
-  const float* zrow; // row mode (large tables): the spec's z' per traditional DNN (global, L1)
+  const float* zrow; // row mode (large tables): the spec's z' per traditional DNN in trad_rows order (global, L1)
   const unsigned* wst;  // per 32-cell window of anytime cells: column-start bits (shared)
   bool any_window;      // ALERT_FLAG_ANY_WINDOW: two-pass window for anytime cells (A/B)
   const int2* su;       // max-accuracy fast scan: units / key lower bounds staged in shared memory
@@ -678,7 +678,7 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
     const float om_s = lin ? x.ompmu * (1.0f - 4e-6f) : 0.0f;
     const float ph_s = lin ? x.phig * T.cap_min * (1.0f - 4e-6f) : 0.0f;
     float4 rw = n_tdnn > 0 ? __ldg(T.trad_rows) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float zn = n_tdnn > 0 ? __ldg(x.zrow + __float_as_int(rw.x)) : 0.f;
+    float zn = n_tdnn > 0 ? __ldg(x.zrow) : 0.f;  // z' in row order: independent of rw
     for (int r = 0; r < n_tdnn; ++r) {
       if (fmaxf(rw.y * mu_es, fmaf(om_s, rw.y, ph_s)) >= t.p2) break;
       const int dn = __float_as_int(rw.x);
@@ -690,7 +690,7 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
       const bool dead = fmaf(mgH, rw.z, Td) > 0.0f;
       if (r + 1 < n_tdnn) {
         rw = __ldg(T.trad_rows + r + 1);
-        zn = __ldg(x.zrow + __float_as_int(rw.x));
+        zn = __ldg(x.zrow + r + 1);
       }
       if (dead) continue;
       const float4* row = sA + dn * P;  // padded table: reads past the row are masked

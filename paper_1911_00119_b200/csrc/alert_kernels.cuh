@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
         }
         float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
         fast_prep(x, tile, fzZ, fzZ + (size_t)n_tiles * n_tdnn, n_tiles, fast_me ? n_tdnn : 0, zpr,
-                  P.fast_rows ? P.zlo + (size_t)si * (n_tdnn + 1) : nullptr);
+                  P.fast_rows ? P.zlo + (size_t)P.n_specs * (n_tdnn + 1) + (size_t)si * n_tdnn : nullptr);
       }
       d = alert_decide<MS>(T, sA, sB, sCol, tile, x, P.kinds, P.flags & ALERT_FLAG_NO_REFINE);
       s = s_of_raw(tr, s_raw);
