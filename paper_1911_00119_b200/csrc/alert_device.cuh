@@ -1139,6 +1139,7 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
   const float elH = -x.e_lo * kPenH;
   const int n_seq = T.n_seq;
   const bool mono = T.any_mono;
+  const bool k_trad = kinds & 1, k_any = kinds & 2;
   // 32-bit shared addresses (no generic-to-shared conversion per cell); the
   // row and the metadata of an entry are independent loads
   const unsigned aqa = (unsigned)__cvta_generic_to_shared(x.sqA);
@@ -1176,9 +1177,11 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
     if (start && lb >= t.p2 && lb > t.p1 + dcut) break;
     // the rest is predicated (no divergent paths inside the loop): a skipped
     // group / chain costs one cell body and moves i
-    const int any = (M.x >> 10) & 1;
-    const bool skip = start && (!((kinds >> any) & 1) || (pp > 0.0f && (!any || mono)));  // group out
-    if (start) acc = A.w;
+    const bool any = (M.x >> 10) & 1;
+    const bool kok = any ? k_any : k_trad;
+    const bool gdead = pp > 0.0f && (!any || mono);
+    const bool skip = start && (!kok || gdead);  // group out
+    acc = start ? A.w : acc;
     const float ph = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
     const float E = energy(A);
     const float pen = fmaxf(fmaf(E, kPenH, elH), pp);
