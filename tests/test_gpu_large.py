@@ -168,3 +168,18 @@ def test_c3_scale_fast_scan_equals_full_scan(c3):
     np.testing.assert_array_equal(a.decoded()["cand"], b.decoded()["cand"])
     np.testing.assert_array_equal(a.records["energy"], b.records["energy"])
     np.testing.assert_array_equal(a.agg[:, :abi.AGG_LEVEL0], b.agg[:, :abi.AGG_LEVEL0])
+
+
+@pytest.mark.parametrize("lanes", [1, 8])
+def test_c4_grid_row_scan_equals_full_scan(lanes):
+    """Row mode on the 64x32 table (rows by smallest cap*t with the energy
+    bound stop, surely-infeasible rows skipped) changes no decision or value
+    against the full scan, at one lane and at the default 8 lanes per stream."""
+    space, specs, packed, ss, sr = _grid(n_traces=32, steps=300)
+    kw = dict(stream_spec=ss, stream_row=sr, records="f32", lanes_per_stream=lanes)
+    fast = A.run_batch(space, A.pack_specs(specs), packed, "alert", **kw)
+    full = A.run_batch(space, A.pack_specs(specs), packed, "alert", flags=abi.FLAG_NO_FAST, **kw)
+    A.get_engine().set_launch(0, 0)
+    np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
+    np.testing.assert_array_equal(fast.records["energy"], full.records["energy"])
+    np.testing.assert_array_equal(fast.agg[:, :abi.AGG_LEVEL0], full.agg[:, :abi.AGG_LEVEL0])
