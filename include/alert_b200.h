@@ -37,7 +37,9 @@
 extern "C" {
 #endif
 
-#define ALERT_ABI_VERSION 2  /* 2: comparison-scheme policies, AlertSpaceDesc.sys_dnn/app_dnn, AlertState.policy_aux, AlertOutputs.fb_*, alert_xi_stats */
+#define ALERT_ABI_VERSION 3  /* 2: comparison-scheme policies, AlertSpaceDesc.sys_dnn/app_dnn, AlertState.policy_aux, AlertOutputs.fb_*, alert_xi_stats
+                               3: goal schedules (AlertTrace.goal_*), AlertOutputs.plan_goal/phi, decision bit 30
+                                  (feasible), alert_baseline_decide / alert_static_choice (per-step comparison schemes) */
 
 /* ---- status codes ------------------------------------------------------ */
 typedef enum AlertStatus {
@@ -155,6 +157,22 @@ typedef struct AlertTrace {
   const int32_t* seg_phase;   /* [n_rows][max_segments] phase id (< ALERT_MAX_PHASES) */
   const double* seg_idle;     /* [n_rows][max_segments] idle_power_true, W     */
   const int32_t* stream_row;  /* [n_streams] or NULL                           */
+  /* Goal changes (optional, NULL = none): per row, segments of constant
+   * constraint spec.  Step n of row r runs under specs[goal_seg_spec[r][g]]
+   * for the segment g with goal_seg_end[r][g-1] <= n < goal_seg_end[r][g]
+   * (the last segment is open-ended); rows with n_goal_segments[r] == 0 use
+   * the stream's spec (stream_spec).  The reference keeps one spec per run;
+   * a change is mirrored there by swapping policy.spec before decide and
+   * measuring against the new spec (SURVEY.md §7 hard part 8; policies.py:97-103,
+   * simulator.py:473-497).  A shared-deadline group that is open when the spec
+   * changes keeps its remaining budget; a new group takes the current spec's
+   * group_size and t_goal.  oracle-static chooses with the spec in force at
+   * the first step of the call (OracleStaticPolicy.begin, policies.py:221-227). */
+  int32_t max_goal_segments;  /* per-row capacity of the goal arrays           */
+  int32_t _pad2;
+  const int32_t* n_goal_segments; /* [n_rows]                                  */
+  const int32_t* goal_seg_end;    /* [n_rows][max_goal_segments] exclusive end  */
+  const int32_t* goal_seg_spec;   /* [n_rows][max_goal_segments] index into specs */
 } AlertTrace;
 
 /* Per-stream policy state, FP64 SoA, read at step_begin and written back at
@@ -204,7 +222,10 @@ enum {
  *   bits 16..17 fallback level        bit 18 deadline_met
  *   bits 19..21 violations (latency, accuracy, energy)
  *   bits 22..25 completed_stage        bit 26 FP64 re-rank used
- *   bits 27..29 phase id                                                   */
+ *   bits 27..29 phase id (low 3 bits)
+ *   bit  30     ConfigDecision.feasible (selector.py:126: level NONE; sys-only:
+ *               some cap predicted on time, policies.py:305-310; oracle-static:
+ *               the choice is eligible, policies.py:257-271; app-only / no-coord: 1) */
 typedef struct AlertOutputs {
   uint32_t* decision;
   void* energy;         /* StepRecord.energy                 */
@@ -222,6 +243,11 @@ typedef struct AlertOutputs {
                             forcing) or -1; NULL = free running.  Same strides. */
   double* fb_latency;   /* StepRecord.fb_latency (FP64, same strides) or NULL */
   double* fb_t_prof;    /* StepRecord.fb_t_prof  (FP64, same strides) or NULL */
+  double* plan_goal;    /* adjusted per-input goal the decision was made for
+                           (simulator.py:479-483; StepRecord.period = plan_goal +
+                           overhead_budget) (FP64, same strides) or NULL */
+  double* phi;          /* idle-power ratio estimate after observe (FP64) or NULL;
+                           with mu / sigma2 it is the state the next decide uses */
 } AlertOutputs;
 
 /* One prediction (predictor.Prediction, predictor.py:36-45), FP64. */
@@ -280,11 +306,30 @@ int alert_observe(AlertContext* ctx, const AlertTable* table, const AlertFilterC
                   void* cuda_stream);
 
 /* OraclePolicy.decide for n (stream, step) items: true slow-down s[n] (FP64),
- * true idle power idle[n], plan goal[n]. */
+ * true idle power idle[n], plan goal[n].  exact (nullable): the chosen
+ * config's _exact_pred (policies.py:172-205: measured latency incl. overhead,
+ * sigma 0, pr 1/0 = deadline met, delivered accuracy, energy). */
 int alert_oracle_decide(AlertContext* ctx, const AlertTable* table, const AlertSpec* specs,
                         int32_t n_specs, const int32_t* stream_spec, const double* s,
                         const double* idle, const double* plan_goal, uint32_t flags,
-                        uint32_t* decision, int64_t n, void* cuda_stream);
+                        uint32_t* decision, AlertPrediction* exact, int64_t n, void* cuda_stream);
+
+/* Comparison schemes step by step (policies.py:211-454).
+ * alert_static_choice = OracleStaticPolicy.begin (policies.py:221-265) for
+ * streams [stream_begin, stream_end) over steps [step_begin, step_end) of the
+ * trace: writes AlertState.policy_aux = candidate | eligible << 16.
+ * alert_baseline_decide = SysOnly / AppOnly / NoCoord / OracleStatic.decide
+ * (policies.py:298-313, 350-368, 392-428, 268-269) for n streams from their
+ * state and plan goal; no-coord updates policy_aux (its controllers' memory).
+ * Decisions packed as in AlertOutputs (bits 0..17, 30).  The filters are
+ * updated with alert_observe. */
+int alert_static_choice(AlertContext* ctx, const AlertTable* table, const AlertSpec* specs, int32_t n_specs,
+                        const int32_t* stream_spec, const AlertTrace* trace, AlertState state,
+                        int64_t stream_begin, int64_t stream_end, int64_t step_begin, int64_t step_end,
+                        void* cuda_stream);
+int alert_baseline_decide(AlertContext* ctx, const AlertTable* table, const AlertSpec* specs, int32_t n_specs,
+                          const int32_t* stream_spec, AlertState state, const double* plan_goal,
+                          int32_t policy, uint32_t* decision, int64_t n, void* cuda_stream);
 
 /* Deterministic fixed-order sum of agg[n_streams][ALERT_AGG_FIELDS] into
  * out[ALERT_AGG_FIELDS] (device), pairwise tree in stream order. */

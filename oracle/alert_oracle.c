@@ -522,6 +522,7 @@ static int cand_index(const Space* s, int i, int j, int target) {
 
 /* OracleStaticPolicy.begin (policies.py:221-265): best fixed candidate over
  * the realized trace; tot_energy / tot_acc are plain running sums. */
+/* returns cand | eligible << 16 (AlertState.policy_aux layout) */
 static int oracle_static_choice(const Space* s, const AlertSpec* spec, int64_t n, const double* sd,
                                 const double* idle) {
   const AlertSpaceDesc* d = s->d;
@@ -565,12 +566,13 @@ static int oracle_static_choice(const Space* s, const AlertSpec* spec, int64_t n
         }
       }
   }
-  return best;
+  return best < 0 ? best : best | (bel << 16);
 }
 
-/* SysOnlyPolicy.decide (policies.py:298-313): cheapest cap predicted on time */
+/* SysOnlyPolicy.decide (policies.py:298-313): cheapest cap predicted on time
+ * (*found = some cap is, policies.py:305-310) */
 static int sys_only_power(const Space* s, const OracleEst* est, const OracleIdle* idl, int dnn, int stage0,
-                          double goal) {
+                          double goal, int* found) {
   const AlertSpaceDesc* d = s->d;
   int bj = -1;
   double be = 0.0;
@@ -580,17 +582,21 @@ static int sys_only_power(const Space* s, const OracleEst* est, const OracleIdle
     double e = oracle_energy_mean(est, idl, d->power_cap[j], t, goal);
     if (bj < 0 || e < be) { be = e; bj = j; }
   }
+  if (found) *found = bj >= 0;
   return bj < 0 ? d->n_powers - 1 : bj;
 }
 
-/* AppOnlyPolicy.decide (policies.py:350-356): best expected-accuracy stage */
-static int app_only_stage(const Space* s, const OracleEst* est, int dnn, int power, double goal) {
+/* AppOnlyPolicy.decide (policies.py:350-356): best expected-accuracy stage
+ * (its expected accuracy in *best_acc) */
+static int app_only_stage(const Space* s, const OracleEst* est, int dnn, int power, double goal,
+                          double* best_acc) {
   int best = 1;
   double ba = -1.0;
   for (int k = 1; k <= s->d->dnn_n_stages[dnn]; ++k) {
     double acc = anytime_acc(s, est, dnn, power, k, goal);
     if (acc > ba) { best = k; ba = acc; }
   }
+  if (best_acc) *best_acc = ba;
   return best;
 }
 
@@ -601,10 +607,11 @@ static int kinds_for(int policy) {
 }
 
 /* simulator.py:461-507 over an injected environment */
-static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig* cfg, int policy,
-                 int64_t n_steps, const double* sd, const double* idle, const int32_t* phase,
+static int run_s(const Space* s, const AlertSpec* specs, const int32_t* spec_index, const AlertFilterConfig* cfg,
+                 int policy, int64_t n_steps, const double* sd, const double* idle, const int32_t* phase,
                  const int32_t* forced, OracleRecord* rec, double* agg, double* state, int state_in,
                  AlertPrediction* preds) {
+  const AlertSpec* spec = spec_index ? &specs[spec_index[0]] : specs; /* spec at begin() */
   const AlertSpaceDesc* d = s->d;
   int kinds = kinds_for(policy);
   /* AlertPolicy.begin, policies.py:86-95 */
@@ -633,8 +640,10 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
   if (aux < 0 && policy == ALERT_POLICY_ORACLE_STATIC) aux = oracle_static_choice(s, spec, n_steps, sd, idle);
   if (aux < 0 && policy == ALERT_POLICY_NO_COORD)
     aux = d->dnn_n_stages[d->app_dnn] | ((d->n_powers - 1) << 8); /* policies.py:385-386 */
-  int has_group = spec->group_size > 0;
   for (int64_t n = 0; n < n_steps; ++n) {
+    const int32_t spec_k = spec_index ? spec_index[n] : 0;
+    spec = &specs[spec_k]; /* policy.spec swapped (goal changes) */
+    int has_group = spec->group_size > 0;
     if (has_group && count == 0) { /* simulator.py:473-478 */
       budget = (double)spec->group_size * spec->t_goal;
       count = spec->group_size;
@@ -646,27 +655,56 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
     int cand;
     int or_cand = -1;
     int32_t or_level = 0;
+    int feasible = 1;
+    /* ConfigDecision.prediction of the decision (latency mean / sigma, pr, accuracy, energy) */
+    double pv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (policy == ALERT_POLICY_ORACLE) {
       cand = oracle_decide_s(s, spec, sd[n], idle[n], goal, &level, &gap);
+      feasible = level == 0;
+      if (cand >= 0) { /* _exact_pred, policies.py:201-205 */
+        int32_t oi, oj, ot;
+        oracle_candidate(d, cand, &oi, &oj, &ot);
+        Exact x = exact_eval(s, spec, sd[n], idle[n], oi, oj, ot, goal);
+        pv[0] = x.latency; pv[2] = x.met ? 1.0 : 0.0; pv[3] = x.delivered; pv[4] = x.energy;
+      }
     } else if (policy == ALERT_POLICY_ORACLE_STATIC) {
-      cand = aux; /* OracleStaticPolicy.decide, policies.py:268-269 */
+      cand = aux & 0xFFFF; /* OracleStaticPolicy.decide, policies.py:268-269 */
+      feasible = (aux >> 16) != 0;
+      pv[2] = feasible ? 1.0 : 0.0; /* _exact_pred(i, j, t, eligible, 0, 0, 0), policies.py:266-271 */
     } else if (policy == ALERT_POLICY_SYS_ONLY) {
-      cand = cand_index(s, d->sys_dnn, sys_only_power(s, &est, &idl, d->sys_dnn, 0, goal), 0);
+      int pj = sys_only_power(s, &est, &idl, d->sys_dnn, 0, goal, &feasible);
+      cand = cand_index(s, d->sys_dnn, pj, 0);
+      double t = t_prof_of(s, d->sys_dnn, 0, pj); /* policies.py:314-320 */
+      pv[0] = est.mu * t; pv[1] = est_sigma(&est) * t; pv[2] = feasible ? 1.0 : 0.0;
+      pv[3] = acc_of(s, d->sys_dnn, 0); pv[4] = oracle_energy_mean(&est, &idl, d->power_cap[pj], t, goal);
     } else if (policy == ALERT_POLICY_APP_ONLY) {
       int pj = d->n_powers - 1;
-      cand = cand_index(s, d->app_dnn, pj, app_only_stage(s, &est, d->app_dnn, pj, goal));
+      double ba;
+      int st = app_only_stage(s, &est, d->app_dnn, pj, goal, &ba);
+      cand = cand_index(s, d->app_dnn, pj, st);
+      double t = t_prof_of(s, d->app_dnn, st - 1, pj); /* policies.py:357-368 */
+      pv[0] = est.mu * t; pv[1] = est_sigma(&est) * t; pv[3] = ba;
     } else if (policy == ALERT_POLICY_NO_COORD) {
       /* NoCoordPolicy.decide (policies.py:392-428): the stage for the old
        * power, the power for the old stage, both from the same feedback (the
        * two estimators receive identical updates, so one is kept) */
       int st_old = aux & 0xff, pj_old = aux >> 8;
-      int st = app_only_stage(s, &est, d->app_dnn, pj_old, goal);
-      int pj = sys_only_power(s, &est, &idl, d->app_dnn, st_old - 1, goal);
+      double ba;
+      int st = app_only_stage(s, &est, d->app_dnn, pj_old, goal, &ba);
+      int pj = sys_only_power(s, &est, &idl, d->app_dnn, st_old - 1, goal, NULL);
       aux = st | (pj << 8);
       cand = cand_index(s, d->app_dnn, pj, st);
+      double t = t_prof_of(s, d->app_dnn, st - 1, pj); /* policies.py:417-428 */
+      pv[0] = est.mu * t; pv[1] = est_sigma(&est) * t; pv[3] = ba;
     } else {
       int np = predict_all_s(s, &est, &idl, spec, goal, preds);
       cand = select_s(s, preds, np, spec, kinds, &level, &gap, &boundary);
+      feasible = level == 0;
+      if (cand >= 0) {
+        const AlertPrediction* p = &preds[cand];
+        pv[0] = p->latency_mean; pv[1] = p->latency_sigma; pv[2] = p->pr_deadline;
+        pv[3] = p->expected_accuracy; pv[4] = p->energy;
+      }
       if (policy == ALERT_POLICY_ALERT_WITH_ORACLE)
         or_cand = oracle_decide_s(s, spec, sd[n], idle[n], goal, &or_level, NULL);
     }
@@ -694,6 +732,9 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
       r->cand = exec_c; r->dnn = di; r->power = pj; r->stage = tg;
       r->level = level; r->completed = o.completed; r->met = m.met; r->phase = ph;
       r->viol_lat = m.vl; r->viol_acc = m.va; r->viol_energy = m.ve; r->or_cand = or_cand;
+      r->feasible = feasible; r->spec_index = spec_k;
+      r->pred_latency_mean = pv[0]; r->pred_latency_sigma = pv[1]; r->pred_pr = pv[2];
+      r->pred_accuracy = pv[3]; r->pred_energy = pv[4];
       r->plan_goal = goal; r->period = period; r->latency = m.latency; r->accuracy = m.delivered;
       r->energy = m.energy; r->fb_latency = o.fb_latency; r->fb_t_prof = o.fb_t_prof; r->s = sd[n];
       r->mu = est.mu; r->sigma2 = est.sigma2; r->k_gain = est.k_gain; r->q_noise = est.q_noise;
@@ -739,19 +780,31 @@ static int run_s(const Space* s, const AlertSpec* spec, const AlertFilterConfig*
   return 0;
 }
 
-int oracle_run(const AlertSpaceDesc* sp, const AlertSpec* spec, const AlertFilterConfig* cfg,
-               int policy, int64_t n_steps, const double* sd, const double* idle,
-               const int32_t* phase, const int32_t* forced, OracleRecord* rec, double* agg,
-               double* state, int state_in) {
+int oracle_run_goals(const AlertSpaceDesc* sp, const AlertSpec* specs, int32_t n_specs,
+                     const int32_t* spec_index, const AlertFilterConfig* cfg, int policy, int64_t n_steps,
+                     const double* sd, const double* idle, const int32_t* phase, const int32_t* forced,
+                     OracleRecord* rec, double* agg, double* state, int state_in) {
+  if (!specs || n_specs < 1) return ALERT_ERR_INVALID_ARGUMENT;
+  if (spec_index)
+    for (int64_t n = 0; n < n_steps; ++n)
+      if (spec_index[n] < 0 || spec_index[n] >= n_specs) return ALERT_ERR_INVALID_ARGUMENT;
   Space s;
   if (space_open(sp, &s)) return ALERT_ERR_INVALID_ARGUMENT;
   AlertPrediction* preds = (AlertPrediction*)malloc(sizeof(AlertPrediction) * (size_t)(s.n_cand + 1));
-  int r = preds ? run_s(&s, spec, cfg, policy, n_steps, sd, idle, phase, forced, rec, agg, state,
+  int r = preds ? run_s(&s, specs, spec_index, cfg, policy, n_steps, sd, idle, phase, forced, rec, agg, state,
                         state_in, preds)
                 : ALERT_ERR_INVALID_ARGUMENT;
   free(preds);
   space_close(&s);
   return r;
+}
+
+int oracle_run(const AlertSpaceDesc* sp, const AlertSpec* spec, const AlertFilterConfig* cfg,
+               int policy, int64_t n_steps, const double* sd, const double* idle,
+               const int32_t* phase, const int32_t* forced, OracleRecord* rec, double* agg,
+               double* state, int state_in) {
+  return oracle_run_goals(sp, spec, 1, NULL, cfg, policy, n_steps, sd, idle, phase, forced, rec, agg, state,
+                          state_in);
 }
 
 /* ---------------------------------------------------------------------- */
@@ -781,6 +834,7 @@ static void* batch_worker(void* arg) {
   double* sd = (double*)malloc(sizeof(double) * (size_t)(len > 0 ? len : 1));
   double* idle = (double*)malloc(sizeof(double) * (size_t)(len > 0 ? len : 1));
   int32_t* ph = (int32_t*)malloc(sizeof(int32_t) * (size_t)(len > 0 ? len : 1));
+  int32_t* gi = (int32_t*)malloc(sizeof(int32_t) * (size_t)(len > 0 ? len : 1));
   AlertPrediction* preds = (AlertPrediction*)malloc(sizeof(AlertPrediction) * (size_t)(s.n_cand + 1));
   for (;;) {
     pthread_mutex_lock(&J->mu);
@@ -800,12 +854,19 @@ static void* batch_worker(void* arg) {
       ph[n] = t->seg_phase[row * t->max_segments + seg];
     }
     int32_t si = J->stream_spec ? J->stream_spec[k] : (int32_t)(k % J->n_specs);
+    const int ng = t->n_goal_segments ? t->n_goal_segments[row] : 0;
+    for (int64_t n = 0; n < len; ++n) { /* goal changes: the row's spec segments */
+      int64_t step = J->step_begin + n;
+      int g = 0;
+      while (g + 1 < ng && step >= t->goal_seg_end[row * t->max_goal_segments + g]) ++g;
+      gi[n] = ng ? t->goal_seg_spec[row * t->max_goal_segments + g] : si;
+    }
     double* st = J->state ? J->state + ORACLE_STATE_FIELDS * k : NULL;
-    int r = run_s(&s, &J->specs[si], J->cfg, J->policy, len, sd, idle, ph, NULL, NULL,
+    int r = run_s(&s, J->specs, gi, J->cfg, J->policy, len, sd, idle, ph, NULL, NULL,
                   J->agg + (size_t)ALERT_AGG_FIELDS * k, st, J->step_begin > 0, preds);
     if (r) J->status = r;
   }
-  free(sd); free(idle); free(ph); free(preds);
+  free(sd); free(idle); free(ph); free(gi); free(preds);
   space_close(&s);
   return NULL;
 }

@@ -37,9 +37,13 @@ typedef struct OracleRecord {
   int32_t cand, dnn, power, stage;      /* stage 0 = None                    */
   int32_t level, completed, met, phase;
   int32_t viol_lat, viol_acc, viol_energy, or_cand;
+  int32_t feasible, spec_index;         /* ConfigDecision.feasible; spec in force (goal changes) */
   double plan_goal, period, latency, accuracy, energy, fb_latency, fb_t_prof, s;
   double mu, sigma2, k_gain, q_noise, innov, phi, m_var;
   double gap, boundary;
+  /* ConfigDecision.prediction: latency_mean, latency_sigma, pr_deadline,
+   * expected_accuracy, energy (predictor.py:36-45) */
+  double pred_latency_mean, pred_latency_sigma, pred_pr, pred_accuracy, pred_energy;
 } OracleRecord;
 
 int oracle_num_candidates(const AlertSpaceDesc* sp);
@@ -85,6 +89,14 @@ int oracle_run(const AlertSpaceDesc* sp, const AlertSpec* spec, const AlertFilte
                int policy, int64_t n_steps, const double* s, const double* idle,
                const int32_t* phase, const int32_t* forced, OracleRecord* rec, double* agg,
                double* state, int state_in);
+/* oracle_run with goal changes: step n runs under specs[spec_index[n]]
+ * (spec_index NULL: specs[0] throughout) — the reference's run loop with
+ * policy.spec swapped before each decide and each input measured against the
+ * spec in force (SURVEY.md §7 hard part 8; simulator.py:473-497). */
+int oracle_run_goals(const AlertSpaceDesc* sp, const AlertSpec* specs, int32_t n_specs,
+                     const int32_t* spec_index, const AlertFilterConfig* cfg, int policy, int64_t n_steps,
+                     const double* s, const double* idle, const int32_t* phase, const int32_t* forced,
+                     OracleRecord* rec, double* agg, double* state, int state_in);
 
 /* Batched runs over a HOST AlertTrace (same layout as the device one) with
  * n_threads POSIX threads, one stream at a time per thread.  agg:

@@ -24,10 +24,11 @@ STATE_FIELDS = 10  # ORACLE_STATE_FIELDS: mu sigma2 k q y phi m budget count aux
 
 RECORD_DTYPE = np.dtype(
     [(n, "<i4") for n in ("cand", "dnn", "power", "stage", "level", "completed", "met", "phase",
-                          "viol_lat", "viol_acc", "viol_energy", "or_cand")]
+                          "viol_lat", "viol_acc", "viol_energy", "or_cand", "feasible", "spec_index")]
     + [(n, "<f8") for n in ("plan_goal", "period", "latency", "accuracy", "energy", "fb_latency",
                             "fb_t_prof", "s", "mu", "sigma2", "k_gain", "q_noise", "innov", "phi",
-                            "m_var", "gap", "boundary")]
+                            "m_var", "gap", "boundary", "pred_latency_mean", "pred_latency_sigma", "pred_pr",
+                            "pred_accuracy", "pred_energy")]
 )
 
 
@@ -86,6 +87,9 @@ def lib():
         L.oracle_run.argtypes = [P(abi.AlertSpaceDesc), P(abi.AlertSpec), P(abi.AlertFilterConfig), C.c_int,
                                  C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_int]
+        L.oracle_run_goals.argtypes = [P(abi.AlertSpaceDesc), C.c_void_p, C.c_int32, C.c_void_p,
+                                       P(abi.AlertFilterConfig), C.c_int, C.c_int64, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
         L.oracle_run_batch.argtypes = [P(abi.AlertSpaceDesc), C.c_void_p, C.c_int32, C.c_void_p,
                                        P(abi.AlertFilterConfig), C.c_int, P(abi.AlertTrace), C.c_int64,
                                        C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int]
@@ -102,9 +106,17 @@ def _packed(space):
 
 
 def run(space, spec, env, policy: str = "alert", kalman=None, forced=None, group_size=None,
-        state=None):
+        state=None, goal_changes=None):
     """simulator.run over an injected environment (TrueEnvironment-like with
-    slowdown / idle_power / phase_index).  Returns (records, agg, state)."""
+    slowdown / idle_power / phase_index).  Returns (records, agg, state).
+    goal_changes: [(input_index, ConstraintSpec), ...] swaps the spec from
+    that input on (oracle_run_goals)."""
+    if goal_changes:
+        specs = [spec] + [c for _, c in goal_changes]
+        idx = np.zeros(len(env.slowdown), np.int32)
+        for k, (n0, _) in enumerate(goal_changes):
+            idx[int(n0):] = k + 1
+        return run_goals(space, pack_specs(specs, group_size), idx, env, policy, kalman, forced, state)
     ps = _packed(space)
     rec = pack_specs([spec], group_size)[0]
     s = np.ascontiguousarray(env.slowdown, dtype=np.float64)
@@ -122,6 +134,28 @@ def run(space, spec, env, policy: str = "alert", kalman=None, forced=None, group
                          int(state is not None))
     if r != 0:
         raise ValueError(f"oracle_run failed: {abi.STATUS_NAMES.get(r, r)}")
+    return records, agg, st
+
+
+def run_goals(space, spec_records, spec_index, env, policy: str = "alert", kalman=None, forced=None, state=None):
+    """oracle_run_goals: step n under spec_records[spec_index[n]]."""
+    ps = _packed(space)
+    specs = np.ascontiguousarray(spec_records)
+    idx = np.ascontiguousarray(spec_index, dtype=np.int32)
+    s = np.ascontiguousarray(env.slowdown, dtype=np.float64)
+    idle = np.ascontiguousarray(env.idle_power, dtype=np.float64)
+    ph = np.ascontiguousarray(env.phase_index, dtype=np.int32)
+    n = len(s)
+    f = None if forced is None else np.ascontiguousarray(forced, dtype=np.int32)
+    records = np.zeros(n, RECORD_DTYPE)
+    agg = np.zeros(abi.AGG_FIELDS, np.float64)
+    st = np.zeros(STATE_FIELDS, np.float64) if state is None else np.array(state, np.float64)
+    cfg = filter_config(kalman)
+    r = lib().oracle_run_goals(C.byref(ps.desc), _p(specs), len(specs), _p(idx), C.byref(cfg), policy_code(policy),
+                               n, _p(s), _p(idle), _p(ph), _p(f), _p(records), _p(agg), _p(st),
+                               int(state is not None))
+    if r != 0:
+        raise ValueError(f"oracle_run_goals failed: {abi.STATUS_NAMES.get(r, r)}")
     return records, agg, st
 
 
@@ -191,6 +225,11 @@ def host_trace_struct(packed, stream_row=None):
         seg_phase=packed.seg_phase.ctypes.data, seg_idle=packed.seg_idle.ctypes.data,
         stream_row=None if sr is None else sr.ctypes.data,
     )
+    if getattr(packed, "goal_n", None) is not None:  # goal changes
+        g = [np.ascontiguousarray(a, np.int32) for a in (packed.goal_n, packed.goal_end, packed.goal_spec)]
+        keep += g
+        t.max_goal_segments = g[1].shape[1]
+        t.n_goal_segments, t.goal_seg_end, t.goal_seg_spec = (a.ctypes.data for a in g)
     return t, keep
 
 

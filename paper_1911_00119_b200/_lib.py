@@ -17,6 +17,7 @@ EXPORTS = (
     "alert_state_init", "alert_run", "alert_decide", "alert_predict", "alert_observe",
     "alert_oracle_decide", "alert_reduce", "alert_set_launch", "alert_get_launch", "alert_launch_count",
     "alert_probe_fp32_peak", "alert_probe_phi32", "alert_xi_stats", "alert_realize", "alert_probe_erfc_rel",
+    "alert_static_choice", "alert_baseline_decide",
 )
 
 
@@ -58,7 +59,10 @@ def load() -> C.CDLL:
     L.alert_decide.argtypes = [V, V, V, C.c_int32, V, abi.AlertState, V, C.c_int32, C.c_uint32, V, C.c_int64, V]
     L.alert_predict.argtypes = [V, V, V, C.c_int32, V, abi.AlertState, V, V, C.c_int64, V]
     L.alert_observe.argtypes = [V, V, P(abi.AlertFilterConfig), abi.AlertState, V, V, V, V, C.c_int64, V]
-    L.alert_oracle_decide.argtypes = [V, V, V, C.c_int32, V, V, V, V, C.c_uint32, V, C.c_int64, V]
+    L.alert_oracle_decide.argtypes = [V, V, V, C.c_int32, V, V, V, V, C.c_uint32, V, V, C.c_int64, V]
+    L.alert_static_choice.argtypes = [V, V, V, C.c_int32, V, P(abi.AlertTrace), abi.AlertState, C.c_int64,
+                                      C.c_int64, C.c_int64, C.c_int64, V]
+    L.alert_baseline_decide.argtypes = [V, V, V, C.c_int32, V, abi.AlertState, V, C.c_int32, V, C.c_int64, V]
     L.alert_reduce.argtypes = [V, V, C.c_int64, V, V]
     L.alert_set_launch.argtypes = [V, C.c_int, C.c_int]
     L.alert_get_launch.argtypes = [V, P(C.c_int), P(C.c_int)]

@@ -6,7 +6,7 @@ import ctypes as C
 
 import numpy as np
 
-ALERT_ABI_VERSION = 2
+ALERT_ABI_VERSION = 3
 
 KIND_TRADITIONAL, KIND_ANYTIME = 0, 1
 MODE_MIN_ENERGY, MODE_MAX_ACCURACY = 0, 1
@@ -101,6 +101,9 @@ class AlertTrace(C.Structure):
         ("step_offset", C.c_int64), ("max_segments", C.c_int32), ("_pad", C.c_int32),
         ("n_segments", C.c_void_p), ("seg_end", C.c_void_p), ("seg_phase", C.c_void_p),
         ("seg_idle", C.c_void_p), ("stream_row", C.c_void_p),
+        # goal changes (ABI 3): per-row spec segments, NULL = none
+        ("max_goal_segments", C.c_int32), ("_pad2", C.c_int32),
+        ("n_goal_segments", C.c_void_p), ("goal_seg_end", C.c_void_p), ("goal_seg_spec", C.c_void_p),
     ]
 
 
@@ -124,6 +127,7 @@ class AlertOutputs(C.Structure):
         ("stream_stride", C.c_int64), ("step_stride", C.c_int64),
         ("agg", C.c_void_p), ("forced", C.c_void_p),
         ("fb_latency", C.c_void_p), ("fb_t_prof", C.c_void_p),
+        ("plan_goal", C.c_void_p), ("phi", C.c_void_p),
     ]
 
 
@@ -157,6 +161,7 @@ def decode_decision(word):
         "completed": ((w >> 22) & 0xF).astype(np.int32),
         "refined": ((w >> 26) & 1).astype(np.int32),
         "phase": ((w >> 27) & 0x7).astype(np.int32),
+        "feasible": ((w >> 30) & 1).astype(np.int32),
     }
 
 

@@ -36,7 +36,7 @@ __device__ __forceinline__ double energy_mean64(double mu, double phi, double p,
 // -> the last (fastest) power.  cell_at(j) = the cell whose t_prof is used.
 template <class F>
 __device__ __forceinline__ int cheapest_power(const DevTable& T, const Cell64* C, const Filter& f, double goal,
-                                              F cell_at) {
+                                              F cell_at, bool* feasible = nullptr) {
   int bj = -1;
   double be = 0.0;
   for (int j = 0; j < T.n_powers; ++j) {
@@ -48,6 +48,7 @@ __device__ __forceinline__ int cheapest_power(const DevTable& T, const Cell64* C
       bj = j;
     }
   }
+  if (feasible) *feasible = bj >= 0;  // policies.py:305-310
   return bj < 0 ? T.n_powers - 1 : bj;
 }
 
@@ -85,10 +86,14 @@ __global__ void static_choice_kernel(const BaseParams P) {
   const long long stream = P.stream_begin + blockIdx.x;
   if (stream >= P.stream_end || P.st.policy_aux[stream] >= 0) return;
   const DevTable& T = P.T;
-  const int si = P.stream_spec ? P.stream_spec[stream] : (int)(stream % P.n_specs);
-  const SpecDev sp = P.specs[si];
   const AlertTrace& tr = P.tr;
   const long long row = tr.stream_row ? tr.stream_row[stream] : stream;
+  // begin() sees the spec in force at the call's first step (goal changes)
+  const int ng = tr.n_goal_segments ? tr.n_goal_segments[row] : 0;
+  const int si = ng ? tr.goal_seg_spec[row * (long long)tr.max_goal_segments +
+                                       goal_seek(tr, row * (long long)tr.max_goal_segments, ng, 0, P.step_begin)]
+                    : (P.stream_spec ? P.stream_spec[stream] : (int)(stream % P.n_specs));
+  const SpecDev sp = P.specs[si];
   const double goal = xsub(sp.t_goal, sp.oh);  // policies.py:227 (no 1 ms floor)
   const double period = xadd(goal, sp.oh);
   const long long n_in = P.step_end - P.step_begin;
@@ -159,7 +164,7 @@ __global__ void static_choice_kernel(const BaseParams P) {
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) P.st.policy_aux[stream] = cell_cand(T.cellB[s_cell[0]]);
+  if (threadIdx.x == 0) P.st.policy_aux[stream] = cell_cand(T.cellB[s_cell[0]]) | (s_el[0] << 16);
 }
 
 // The closed loop of a comparison scheme (simulator.run, simulator.py:461-507),
@@ -170,10 +175,14 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
   if (stream >= P.stream_end) return;
   const DevTable& T = P.T;
   const Cell64* C = T.c64;
-  const int si = P.stream_spec ? P.stream_spec[stream] : (int)(stream % P.n_specs);
-  const SpecDev sp = P.specs[si];
   const AlertTrace& tr = P.tr;
   const long long row = tr.stream_row ? tr.stream_row[stream] : stream;
+  const int ng = tr.n_goal_segments ? tr.n_goal_segments[row] : 0;  // goal changes
+  const long long gseg0 = row * (long long)tr.max_goal_segments;
+  int gseg = ng ? goal_seek(tr, gseg0, ng, 0, P.step_begin) : 0;
+  int gend = ng ? goal_end(tr, gseg0, ng, gseg) : 0x7fffffff;
+  SpecDev sp = P.specs[ng ? tr.goal_seg_spec[gseg0 + gseg]
+                          : (P.stream_spec ? P.stream_spec[stream] : (int)(stream % P.n_specs))];
   Filter f;
   f.mu = P.st.mu[stream];
   f.sigma2 = P.st.sigma2[stream];
@@ -189,7 +198,8 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
   int aux = P.st.policy_aux ? P.st.policy_aux[stream] : -1;
   const int Pw = T.n_powers;
   if (POL == ALERT_POLICY_NO_COORD && aux < 0) aux = T.app_stages | ((Pw - 1) << 8);  // policies.py:385-386
-  const int static_cell = POL == ALERT_POLICY_ORACLE_STATIC ? T.cell_of_cand[aux] : -1;
+  const int static_cell = POL == ALERT_POLICY_ORACLE_STATIC ? T.cell_of_cand[aux & 0xFFFF] : -1;
+  const bool static_ok = POL == ALERT_POLICY_ORACLE_STATIC && (aux >> 16) != 0;  // eligible
 
   const int nseg = tr.n_segments[row];
   const long long seg0 = row * tr.max_segments;
@@ -215,6 +225,11 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
       idle = tr.seg_idle[seg0 + seg];
       if (agg) open_segment(G, agg, phase);
     }
+    if (n >= gend) {  // goal change (policy.spec swapped)
+      gseg = goal_seek(tr, gseg0, ng, gseg, n);
+      gend = goal_end(tr, gseg0, ng, gseg);
+      sp = P.specs[tr.goal_seg_spec[gseg0 + gseg]];
+    }
     double goal, period;  // adjust_goal (selector.py:48-70), simulator.py:473-483
     if (sp.group_size > 0) {
       if (count == 0) {
@@ -228,10 +243,12 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
       period = sp.period0;
     }
     int cell;
+    bool feasible = true;
     if (POL == ALERT_POLICY_ORACLE_STATIC) {
       cell = static_cell;
+      feasible = static_ok;
     } else if (POL == ALERT_POLICY_SYS_ONLY) {
-      cell = T.sys_cells[cheapest_power(T, C, f, goal, [&](int j) { return T.sys_cells[j]; })];
+      cell = T.sys_cells[cheapest_power(T, C, f, goal, [&](int j) { return T.sys_cells[j]; }, &feasible)];
     } else if (POL == ALERT_POLICY_APP_ONLY) {
       cell = T.app_first[Pw - 1] + best_stage(C, T.app_first[Pw - 1], T.app_stages, f, goal) - 1;
     } else {  // no-coord: stage for the old power, power for the old stage
@@ -261,10 +278,12 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
       const long long oidx = stream * out.stream_stride + n * out.step_stride;
       out.fb_latency[oidx] = o.fb_latency;
       out.fb_t_prof[oidx] = o.fb_t_prof;
+      if (out.plan_goal) out.plan_goal[oidx] = goal;
+      if (out.phi) out.phi[oidx] = f.phi;
     }
     if (out.decision) {
       const long long oidx = stream * out.stream_stride + n * out.step_stride;
-      out.decision[oidx] = pack_decision(cell_cand(T.cellB[cell]), 0, o, false, phase);
+      out.decision[oidx] = pack_decision(cell_cand(T.cellB[cell]), 0, o, false, phase, feasible);
       if (out.record_dtype == ALERT_DTYPE_F64) {
         if (out.energy) static_cast<double*>(out.energy)[oidx] = o.energy;
         if (out.accuracy) static_cast<double*>(out.accuracy)[oidx] = o.delivered;
@@ -306,6 +325,44 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
     agg[ALERT_AGG_ACC] = G.a; agg[ALERT_AGG_ACC_C] = G.ac;
     agg[ALERT_AGG_LEVEL0] += steps;  // the comparison schemes never fall back (level NONE)
   }
+}
+
+// SysOnly / AppOnly / NoCoord / OracleStatic .decide for n streams (one
+// thread each) from their filter state and plan goal: the same device
+// functions as the fused loop.  No-coord writes its new (stage, power) memory.
+__global__ void baseline_decide_kernel(const DevTable T, const SpecDev* specs, int n_specs, const int32_t* stream_spec,
+                                       AlertState st, const double* plan_goal, int policy, uint32_t* decision,
+                                       long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  (void)specs; (void)n_specs; (void)stream_spec;  // the schemes read only the plan goal (policies.py:298-428)
+  const Cell64* C = T.c64;
+  Filter f;
+  f.mu = st.mu[i];
+  f.sigma2 = st.sigma2[i];
+  f.phi = st.phi[i];
+  const double goal = plan_goal[i];
+  const int Pw = T.n_powers;
+  int cell;
+  bool feasible = true;
+  if (policy == ALERT_POLICY_ORACLE_STATIC) {
+    const int aux = st.policy_aux[i];
+    cell = T.cell_of_cand[aux & 0xFFFF];
+    feasible = (aux >> 16) != 0;
+  } else if (policy == ALERT_POLICY_SYS_ONLY) {
+    cell = T.sys_cells[cheapest_power(T, C, f, goal, [&](int j) { return T.sys_cells[j]; }, &feasible)];
+  } else if (policy == ALERT_POLICY_APP_ONLY) {
+    cell = T.app_first[Pw - 1] + best_stage(C, T.app_first[Pw - 1], T.app_stages, f, goal) - 1;
+  } else {
+    int aux = st.policy_aux[i];
+    if (aux < 0) aux = T.app_stages | ((Pw - 1) << 8);  // policies.py:385-386
+    const int st_old = aux & 0xff, pj_old = aux >> 8;
+    const int stg = best_stage(C, T.app_first[pj_old], T.app_stages, f, goal);
+    const int pj = cheapest_power(T, C, f, goal, [&](int j) { return T.app_first[j] + st_old - 1; });
+    st.policy_aux[i] = stg | (pj << 8);
+    cell = T.app_first[pj] + stg - 1;
+  }
+  decision[i] = (uint32_t)cell_cand(T.cellB[cell]) | ((uint32_t)feasible << 30);
 }
 
 }  // namespace alert

@@ -13,8 +13,15 @@
 #include "alert_baselines.cuh"
 
 #include <curand_kernel.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys / ncu --nvtx
 
 using namespace alert;
+
+// NVTX range for the duration of an entry point (SURVEY §5 tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ==========================================================================
 // error plumbing
@@ -900,6 +907,7 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
               int32_t n_specs, const int32_t* stream_spec, const AlertTrace* tr, AlertState st,
               const AlertOutputs* out, int32_t policy, uint32_t flags, int64_t stream_begin, int64_t stream_end,
               int64_t step_begin, int64_t step_end, void* cuda_stream) {
+  NvtxRange nvtx_range("alert_run");
   if (!ctx || !tb || !cfg || !tr || !out) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: NULL argument");
   int r = check_specs(specs, n_specs);
   if (r) return r;
@@ -916,6 +924,8 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   if (!kinds) return fail(ALERT_ERR_NO_CANDIDATE, "alert_run: space has no DNN of the policy's kinds");
   if (!tr->slowdown || !tr->n_segments || !tr->seg_end || !tr->seg_phase || !tr->seg_idle || tr->max_segments < 1)
     return fail(ALERT_ERR_INVALID_TRACE, "alert_run: incomplete trace description");
+  if (tr->n_goal_segments && (!tr->goal_seg_end || !tr->goal_seg_spec || tr->max_goal_segments < 1))
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_run: incomplete goal-change description");
   if (tr->slowdown_dtype != ALERT_DTYPE_F32 && tr->slowdown_dtype != ALERT_DTYPE_F64)
     return fail(ALERT_ERR_INVALID_TRACE, "alert_run: unknown slowdown dtype");
   if (step_begin < tr->step_offset || step_end < step_begin || step_end > tr->step_offset + tr->n_steps)
@@ -996,6 +1006,76 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   cudaFreeAsync(dspecs, s);
   if (dzlo) cudaFreeAsync(dzlo, s);
   if (r) return r;
+  ctx->launches++;
+  return ALERT_OK;
+}
+
+int alert_static_choice(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs, int32_t n_specs,
+                        const int32_t* stream_spec, const AlertTrace* tr, AlertState st, int64_t stream_begin,
+                        int64_t stream_end, int64_t step_begin, int64_t step_end, void* cuda_stream) {
+  if (!ctx || !tb || !tr) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_static_choice: NULL argument");
+  int r = check_specs(specs, n_specs);
+  if (r) return r;
+  if (!st.policy_aux) return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_static_choice: needs AlertState.policy_aux");
+  if (!tr->slowdown || !tr->n_segments || !tr->seg_end || !tr->seg_phase || !tr->seg_idle || tr->max_segments < 1)
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_static_choice: incomplete trace description");
+  if (tr->n_goal_segments && (!tr->goal_seg_end || !tr->goal_seg_spec || tr->max_goal_segments < 1))
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_static_choice: incomplete goal-change description");
+  if (step_begin < tr->step_offset || step_end <= step_begin || step_end > tr->step_offset + tr->n_steps)
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_static_choice: step range outside the trace buffer");
+  if (stream_begin < 0 || stream_end < stream_begin || stream_end > 0x7fffffffLL)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_static_choice: bad stream range");
+  if (!tr->stream_row && stream_end > tr->n_rows)
+    return fail(ALERT_ERR_INVALID_TRACE, "alert_static_choice: more streams than trace rows and no stream_row map");
+  if (stream_end == stream_begin) return ALERT_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  SpecDev* dspecs = nullptr;
+  r = upload_specs(specs, n_specs, tb, s, &dspecs);
+  if (r) return r;
+  BaseParams B{};
+  B.T = tb->dev;
+  B.specs = dspecs;
+  B.n_specs = n_specs;
+  B.stream_spec = stream_spec;
+  B.tr = *tr;
+  B.st = st;
+  B.policy = ALERT_POLICY_ORACLE_STATIC;
+  B.stream_begin = stream_begin;
+  B.stream_end = stream_end;
+  B.step_begin = step_begin;
+  B.step_end = step_end;
+  static_choice_kernel<<<(unsigned)(stream_end - stream_begin), 128, 0, s>>>(B);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(dspecs, s);
+  if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("static_choice_kernel: ") + cudaGetErrorString(e));
+  ctx->launches++;
+  return ALERT_OK;
+}
+
+int alert_baseline_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs, int32_t n_specs,
+                          const int32_t* stream_spec, AlertState st, const double* plan_goal, int32_t policy,
+                          uint32_t* decision, int64_t n, void* cuda_stream) {
+  if (!ctx || !tb || !plan_goal || !decision)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_baseline_decide: NULL argument");
+  int r = check_specs(specs, n_specs);
+  if (r) return r;
+  if (policy < ALERT_POLICY_ORACLE_STATIC || policy > ALERT_POLICY_NO_COORD)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_baseline_decide: policy must be a comparison scheme");
+  if (policy == ALERT_POLICY_SYS_ONLY && !tb->dev.sys_cells)
+    return fail(ALERT_ERR_NO_CANDIDATE, "alert_baseline_decide: sys-only needs a traditional DNN");
+  if ((policy == ALERT_POLICY_APP_ONLY || policy == ALERT_POLICY_NO_COORD) && !tb->dev.app_first)
+    return fail(ALERT_ERR_NO_CANDIDATE, "alert_baseline_decide: space has no anytime DNN");
+  if ((policy == ALERT_POLICY_ORACLE_STATIC || policy == ALERT_POLICY_NO_COORD) && !st.policy_aux)
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_baseline_decide: this policy needs AlertState.policy_aux");
+  if ((policy != ALERT_POLICY_ORACLE_STATIC) && (!st.mu || !st.sigma2 || !st.phi))
+    return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_baseline_decide: NULL state array");
+  if (n <= 0) return n < 0 ? fail(ALERT_ERR_INVALID_ARGUMENT, "alert_baseline_decide: n < 0") : ALERT_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  baseline_decide_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(tb->dev, nullptr, n_specs, stream_spec, st,
+                                                                     plan_goal, policy, decision, n);
+  CUDA_TRY(cudaGetLastError());
   ctx->launches++;
   return ALERT_OK;
 }
@@ -1099,7 +1179,7 @@ int alert_observe(AlertContext* ctx, const AlertTable* tb, const AlertFilterConf
 
 int alert_oracle_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs, int32_t n_specs,
                         const int32_t* stream_spec, const double* sd, const double* idle, const double* plan_goal,
-                        uint32_t flags, uint32_t* decision, int64_t n, void* cuda_stream) {
+                        uint32_t flags, uint32_t* decision, AlertPrediction* exact, int64_t n, void* cuda_stream) {
   if (!ctx || !tb || !sd || !idle || !plan_goal || !decision)
     return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_oracle_decide: NULL argument");
   int r = check_specs(specs, n_specs);
@@ -1112,15 +1192,14 @@ int alert_oracle_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec
   if (r) return r;
   int W = pick_lanes(ctx, tb);
   int tpb = ctx->tpb;
-  unsigned blocks = (unsigned)((n * W + tpb - 1) / tpb);
   cudaError_t e;
   switch (W) {
-    case 1: e = launch_oracle<1>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
-    case 2: e = launch_oracle<2>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
-    case 4: e = launch_oracle<4>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
-    case 8: e = launch_oracle<8>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
-    case 16: e = launch_oracle<16>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
-    default: e = launch_oracle<32>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, n, tpb, flags, s); break;
+    case 1: e = launch_oracle<1>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, exact, n, tpb, flags, s); break;
+    case 2: e = launch_oracle<2>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, exact, n, tpb, flags, s); break;
+    case 4: e = launch_oracle<4>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, exact, n, tpb, flags, s); break;
+    case 8: e = launch_oracle<8>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, exact, n, tpb, flags, s); break;
+    case 16: e = launch_oracle<16>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, exact, n, tpb, flags, s); break;
+    default: e = launch_oracle<32>(tb->dev, dspecs, n_specs, stream_spec, sd, idle, plan_goal, decision, exact, n, tpb, flags, s); break;
   }
   cudaFreeAsync(dspecs, s);
   if (e != cudaSuccess) return fail(ALERT_ERR_CUDA, std::string("oracle_decide_kernel: ") + cudaGetErrorString(e));

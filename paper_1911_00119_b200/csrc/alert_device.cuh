@@ -1897,10 +1897,11 @@ __device__ __forceinline__ Decision oracle_decide(const DevTable& T, const float
   return oracle_decide_t<0>(T, sA, sB, C, sCol, tile, sp, o);
 }
 
-__device__ __forceinline__ uint32_t pack_decision(int cand, int level, const Outcome& o, bool refined, int phase) {
+__device__ __forceinline__ uint32_t pack_decision(int cand, int level, const Outcome& o, bool refined, int phase,
+                                                  bool feasible) {
   return (uint32_t)cand | ((uint32_t)level << 16) | ((uint32_t)o.met << 18) | ((uint32_t)o.vl << 19) |
          ((uint32_t)o.va << 20) | ((uint32_t)o.ve << 21) | ((uint32_t)(o.completed & 0xF) << 22) |
-         ((uint32_t)refined << 26) | ((uint32_t)(phase & 0x7) << 27);
+         ((uint32_t)refined << 26) | ((uint32_t)(phase & 0x7) << 27) | ((uint32_t)feasible << 30);
 }
 
 }  // namespace alert

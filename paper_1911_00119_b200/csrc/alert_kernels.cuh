@@ -47,9 +47,19 @@ struct RunParams {
 // changes, by group specs, and once per step for the idle power.
 struct ColdState {
   double budget, idle;
-  long long seg0;
+  long long seg0, gseg0;
   int count, seg, nseg, phase;
+  int gseg, ngseg, gend, si;  // goal-change cursor (AlertTrace.goal_*), current spec index
 };
+
+// Goal changes (AlertTrace.goal_*): the segment of `row` holding step n and its end.
+__device__ __forceinline__ int goal_seek(const AlertTrace& tr, long long gseg0, int ng, int g, long long n) {
+  while (g + 1 < ng && n >= tr.goal_seg_end[gseg0 + g]) ++g;
+  return g;
+}
+__device__ __forceinline__ int goal_end(const AlertTrace& tr, long long gseg0, int ng, int g) {
+  return g + 1 < ng ? tr.goal_seg_end[gseg0 + g] : 0x7fffffff;
+}
 
 // Shared-memory layout of run_kernel (host and device compute it identically).
 struct SmemLayout {
@@ -233,32 +243,42 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   ColdState& cs = sCold[threadIdx.x];
   const unsigned sv_tile = (unsigned)__cvta_generic_to_shared(sV + (size_t)tid * T.n_cells);
 
-  const int si = P.stream_spec ? P.stream_spec[stream] : (int)(stream_ll % P.n_specs);
-  // the stream's spec, copied once into the tile's shared slot (all per-step
-  // spec reads are then shared-memory loads)
-  SpecDev* spec = sSpec + tid;
-  {
-    const float4* src = reinterpret_cast<const float4*>(P.specs + si);
-    float4* dst = reinterpret_cast<float4*>(spec);
-    for (int k = tile.thread_rank(); k < (int)(sizeof(SpecDev) / 16); k += W) dst[k] = src[k];
-    tile.sync();
-  }
   const AlertTrace& tr = P.tr;
   const long long row = tr.stream_row ? tr.stream_row[stream] : stream_ll;
-  // min-energy fast scan: the stream's z-thresholds, copied once into the
-  // tile's interleaved shared slots (element d at [d * n_tiles + tile])
-  const bool fast = P.zlo && (spec->mode == ALERT_MODE_MIN_ENERGY || T.units);
-  const bool fast_me = fast && spec->mode == ALERT_MODE_MIN_ENERGY;  // per-DNN thresholds needed
+  // goal changes: the row's spec segment at step_begin overrides stream_spec
+  cs.ngseg = tr.n_goal_segments ? tr.n_goal_segments[row] : 0;
+  cs.gseg0 = row * (long long)tr.max_goal_segments;
+  cs.gseg = cs.ngseg ? goal_seek(tr, cs.gseg0, cs.ngseg, 0, P.step_begin) : 0;
+  cs.gend = cs.ngseg ? goal_end(tr, cs.gseg0, cs.ngseg, cs.gseg) : 0x7fffffff;
+  cs.si = cs.ngseg ? tr.goal_seg_spec[cs.gseg0 + cs.gseg]
+                   : (P.stream_spec ? P.stream_spec[stream] : (int)(stream_ll % P.n_specs));
+  // the stream's spec, copied into the tile's shared slot (all per-step spec
+  // reads are then shared-memory loads); again at every goal change.
+  // min-energy fast scan: the spec's z-thresholds, copied into the tile's
+  // interleaved shared slots (element d at [d * n_tiles + tile])
+  SpecDev* spec = sSpec + tid;
+  bool fast = false, fast_me = false;
   float zpr = -kInfF;
-  if (fast) {
-    const float* zrow = P.zlo + (size_t)si * (n_tdnn + 1);
-    zpr = zrow[n_tdnn];
-    if (!P.fast_rows && fast_me) {
-      float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
-      for (int d = tile.thread_rank(); d < n_tdnn; d += W) fzZ[d * n_tiles] = zrow[d];
-      if (W > 1) tile.sync();
+  auto stage_spec = [&](int si) {
+    const float4* src = reinterpret_cast<const float4*>(P.specs + si);
+    float4* dst = reinterpret_cast<float4*>(spec);
+    tile.sync();  // every lane is done with the previous spec
+    for (int k = tile.thread_rank(); k < (int)(sizeof(SpecDev) / 16); k += W) dst[k] = src[k];
+    tile.sync();
+    fast = P.zlo && (spec->mode == ALERT_MODE_MIN_ENERGY || T.units);
+    fast_me = fast && spec->mode == ALERT_MODE_MIN_ENERGY;  // per-DNN thresholds needed
+    zpr = -kInfF;
+    if (fast) {
+      const float* zrow = P.zlo + (size_t)si * (n_tdnn + 1);
+      zpr = zrow[n_tdnn];
+      if (!P.fast_rows && fast_me) {
+        float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
+        for (int d = tile.thread_rank(); d < n_tdnn; d += W) fzZ[d * n_tiles] = zrow[d];
+        if (W > 1) tile.sync();
+      }
     }
-  }
+  };
+  stage_spec(cs.si);
 
   Filter f;
   f.mu = P.st.mu[stream];
@@ -288,7 +308,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
     cs.phase = tr.seg_phase[seg0 + seg];
     cs.idle = tr.seg_idle[seg0 + seg];
   }
-  int cur_end = cs.seg + 1 < cs.nseg ? tr.seg_end[cs.seg0 + cs.seg] : 0x7fffffff;
+  int cur_end = min(cs.seg + 1 < cs.nseg ? tr.seg_end[cs.seg0 + cs.seg] : 0x7fffffff, cs.gend);
   if (P.ratio_smem) fill_ratios(T, tile, sRatio + (size_t)tid * T.n_powers, cs.idle);
 
   const bool has_agg = P.out.agg != nullptr;
@@ -324,18 +344,29 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       sptr += tr.step_stride * esz;
       prefetch_s(slot_sa + 8u * (par ^ 1u), sptr, f64);
     }
-    if (n >= cur_end) {  // segment change (rare): cursor, phase, idle power
+    if (n >= cur_end) {  // segment change (rare): cursor, phase, idle power; goal change
       int seg = cs.seg;
       const int nseg = cs.nseg;
       const long long seg0 = cs.seg0;
-      if (has_agg && writer) flush_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase);
-      while (seg + 1 < nseg && n >= tr.seg_end[seg0 + seg]) ++seg;
-      cs.seg = seg;
-      cs.phase = tr.seg_phase[seg0 + seg];
-      cs.idle = tr.seg_idle[seg0 + seg];
-      cur_end = seg + 1 < nseg ? tr.seg_end[seg0 + seg] : 0x7fffffff;
-      if (P.ratio_smem) fill_ratios(T, tile, sRatio + (size_t)tid * T.n_powers, cs.idle);
-      if (has_agg && writer) open_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase);
+      if (seg + 1 < nseg && n >= tr.seg_end[seg0 + seg]) {
+        if (has_agg && writer) flush_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase);
+        while (seg + 1 < nseg && n >= tr.seg_end[seg0 + seg]) ++seg;
+        cs.seg = seg;
+        cs.phase = tr.seg_phase[seg0 + seg];
+        cs.idle = tr.seg_idle[seg0 + seg];
+        if (P.ratio_smem) fill_ratios(T, tile, sRatio + (size_t)tid * T.n_powers, cs.idle);
+        if (has_agg && writer) open_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase);
+      }
+      if (n >= cs.gend) {  // goal change: the row's next spec (policy.spec swapped)
+        cs.gseg = goal_seek(tr, cs.gseg0, cs.ngseg, cs.gseg, n);
+        cs.gend = goal_end(tr, cs.gseg0, cs.ngseg, cs.gseg);
+        const int si = tr.goal_seg_spec[cs.gseg0 + cs.gseg];
+        if (si != cs.si) {
+          cs.si = si;
+          stage_spec(si);
+        }
+      }
+      cur_end = min(seg + 1 < nseg ? tr.seg_end[seg0 + seg] : 0x7fffffff, cs.gend);
     }
     // adjust_goal (selector.py:48-70) with group budgets (simulator.py:473-483)
     double goal, period;
@@ -377,7 +408,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
         }
         float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
         fast_prep(x, tile, fzZ, fzZ + (size_t)n_tiles * n_tdnn, n_tiles, fast_me ? n_tdnn : 0, zpr,
-                  P.fast_rows ? P.zlo + (size_t)P.n_specs * (n_tdnn + 1) + (size_t)si * n_tdnn : nullptr);
+                  P.fast_rows ? P.zlo + (size_t)P.n_specs * (n_tdnn + 1) + (size_t)cs.si * n_tdnn : nullptr);
       }
       d = alert_decide<MS>(T, sA, sB, sCol, tile, x, P.kinds, P.flags & ALERT_FLAG_NO_REFINE);
       s = s_of_raw(tr, s_raw);
@@ -401,14 +432,16 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       cs.count -= 1;
     }
     const AlertOutputs& out = P.out;
-    if (writer && out.fb_latency) {  // StepRecord feedback pair (xi diagnostics)
+    if (writer && out.fb_latency) {  // StepRecord feedback pair (xi diagnostics), goal, phi
       const long long oidx = stream_ll * out.stream_stride + (long long)n * out.step_stride;
       out.fb_latency[oidx] = o.fb_latency;
       out.fb_t_prof[oidx] = o.fb_t_prof;
+      if (out.plan_goal) out.plan_goal[oidx] = goal;
+      if (out.phi) out.phi[oidx] = f.phi;
     }
     if (writer && out.decision) {
       const long long oidx = stream_ll * out.stream_stride + (long long)n * out.step_stride;
-      out.decision[oidx] = pack_decision(cell_cand(sB[d.cell]), d.level, o, d.refined, cs.phase);
+      out.decision[oidx] = pack_decision(cell_cand(sB[d.cell]), d.level, o, d.refined, cs.phase, d.level == 0);
       if (out.record_dtype == ALERT_DTYPE_F64) {
         if (out.energy) static_cast<double*>(out.energy)[oidx] = o.energy;
         if (out.accuracy) static_cast<double*>(out.accuracy)[oidx] = o.delivered;
@@ -445,7 +478,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       }
       if (writer && out.oracle_decision)
         out.oracle_decision[stream_ll * out.stream_stride + (long long)n * out.step_stride] =
-            pack_decision(cell_cand(sB[od.cell]), od.level, oo, false, cs.phase);
+            pack_decision(cell_cand(sB[od.cell]), od.level, oo, false, cs.phase, od.level == 0);
     }
   }
   if (!writer) return;
@@ -516,19 +549,34 @@ __global__ void __launch_bounds__(256) decide_kernel(const StepParams P, uint32_
   make_ctx(x, spec, T.c64, P.st.mu[i], P.st.sigma2[i], P.st.phi[i], P.goal[i], P.flags & ALERT_FLAG_FP64_ALL);
   Decision d = alert_decide(T, sA, sB, sCol, tile, x, P.kinds, P.flags & ALERT_FLAG_NO_REFINE);
   if (tile.thread_rank() == 0)
-    decision[i] = (uint32_t)cell_cand(sB[d.cell]) | ((uint32_t)d.level << 16) | ((uint32_t)d.refined << 26);
+    decision[i] = (uint32_t)cell_cand(sB[d.cell]) | ((uint32_t)d.level << 16) | ((uint32_t)d.refined << 26) |
+                  ((uint32_t)(d.level == 0) << 30);
 }
 
 template <int W>
 __global__ void oracle_decide_kernel(const DevTable T, const SpecDev* specs, int n_specs, const int32_t* stream_spec,
                                      const double* s, const double* idle, const double* goal, uint32_t* decision,
-                                     long long n, bool fp64_all) {
+                                     AlertPrediction* exact, long long n, bool fp64_all) {
   auto tile = cg::tiled_partition<W>(cg::this_thread_block());
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;
   if (i >= n) return;
   const int si = stream_spec ? stream_spec[i] : (int)(i % n_specs);
   Decision d = oracle_decide(T, T.cellA, T.cellB, T.c64, T.any_cols, tile, specs + si, s[i], idle[i], goal[i], fp64_all);
-  if (tile.thread_rank() == 0) decision[i] = (uint32_t)cell_cand(T.cellB[d.cell]) | ((uint32_t)d.level << 16);
+  if (tile.thread_rank() == 0) {
+    decision[i] = (uint32_t)cell_cand(T.cellB[d.cell]) | ((uint32_t)d.level << 16) | ((uint32_t)(d.level == 0) << 30);
+    if (exact) {  // _exact_pred of the choice (policies.py:172-205): its exact outcome, period = goal + overhead
+      const Outcome o = execute_measure(T.cellB, T.c64, specs + si, d.cell, s[i], goal[i],
+                                        xadd(goal[i], specs[si].oh), idle[i]);
+      AlertPrediction p;
+      p.latency_mean = o.latency;
+      p.latency_sigma = 0.0;
+      p.pr_deadline = o.met ? 1.0 : 0.0;
+      p.expected_accuracy = o.delivered;
+      p.energy = o.energy;
+      p.dnn_index = p.power_index = p.target_stage = p._pad = 0;
+      exact[i] = p;
+    }
+  }
 }
 
 
@@ -540,7 +588,7 @@ cudaError_t launch_decide(const StepParams& P, uint32_t* out, int tpb, size_t sm
 template <int W>
 cudaError_t launch_oracle(const DevTable& T, const SpecDev* specs, int n_specs, const int32_t* stream_spec,
                           const double* s, const double* idle, const double* goal, uint32_t* decision,
-                          long long n, int tpb, unsigned flags, cudaStream_t st);
+                          AlertPrediction* exact, long long n, int tpb, unsigned flags, cudaStream_t st);
 
 template <class K>
 inline cudaError_t set_smem(K kern, size_t smem) {
@@ -579,11 +627,11 @@ inline cudaError_t set_smem(K kern, size_t smem) {
   template <>                                                                                         \
   cudaError_t launch_oracle<W>(const DevTable& T, const SpecDev* specs, int n_specs,                  \
                                const int32_t* stream_spec, const double* s, const double* idle,       \
-                               const double* goal, uint32_t* decision, long long n, int tpb,         \
-                               unsigned flags, cudaStream_t st) {                                     \
+                               const double* goal, uint32_t* decision, AlertPrediction* exact,        \
+                               long long n, int tpb, unsigned flags, cudaStream_t st) {              \
     long long blocks = (n * W + tpb - 1) / tpb;                                                       \
     oracle_decide_kernel<W><<<(unsigned)blocks, tpb, 0, st>>>(T, specs, n_specs, stream_spec, s, idle, goal, \
-                                                             decision, n, flags & ALERT_FLAG_FP64_ALL);  \
+                                                             decision, exact, n, flags & ALERT_FLAG_FP64_ALL); \
     return cudaGetLastError();                                                                        \
   }
 

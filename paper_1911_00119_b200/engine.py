@@ -42,6 +42,9 @@ class DeviceTrace:
     stream_row: object = None
     step_offset: int = 0
     total_steps: int | None = None  # steps of the whole trace when this buffer is a chunk
+    goal_n: object = None     # goal changes (AlertTrace.goal_*), None = none
+    goal_end: object = None
+    goal_spec: object = None
 
     @property
     def n_rows(self) -> int:
@@ -62,7 +65,20 @@ class DeviceTrace:
             n_segments=self.n_segments.data_ptr(), seg_end=self.seg_end.data_ptr(),
             seg_phase=self.seg_phase.data_ptr(), seg_idle=self.seg_idle.data_ptr(),
             stream_row=_ptr(self.stream_row),
+            max_goal_segments=0 if self.goal_end is None else int(self.goal_end.shape[1]), _pad2=0,
+            n_goal_segments=_ptr(self.goal_n), goal_seg_end=_ptr(self.goal_end), goal_seg_spec=_ptr(self.goal_spec),
         )
+
+    def with_goal_changes(self, goal_n, goal_end, goal_spec) -> "DeviceTrace":
+        """This trace with per-row goal changes (host arrays from
+        trace.pack_goal_changes) uploaded next to it."""
+        torch = _torch()
+        d = self.slowdown.device
+        from dataclasses import replace
+
+        return replace(self, goal_n=torch.from_numpy(np.ascontiguousarray(goal_n, np.int32)).to(d),
+                       goal_end=torch.from_numpy(np.ascontiguousarray(goal_end, np.int32)).to(d),
+                       goal_spec=torch.from_numpy(np.ascontiguousarray(goal_spec, np.int32)).to(d))
 
 
 class GpuTable:
@@ -99,6 +115,7 @@ class Engine:
         check(load().alert_create(C.byref(h), device))
         self.ctx = h
         self._tables = {}
+        self._launch_args = (0, 0)  # alert_set_launch arguments in effect (0 = library default)
 
     def __del__(self):
         try:
@@ -109,8 +126,14 @@ class Engine:
             pass
 
     # -- configuration --------------------------------------------------------
-    def set_launch(self, lanes_per_stream: int = 0, threads_per_block: int = 0) -> None:
+    def set_launch(self, lanes_per_stream: int = 0, threads_per_block: int = 0) -> tuple[int, int]:
+        """Set the launch geometry; returns the previous arguments (for restore_launch)."""
         check(load().alert_set_launch(self.ctx, lanes_per_stream, threads_per_block))
+        prev, self._launch_args = self._launch_args, (lanes_per_stream, threads_per_block)
+        return prev
+
+    def restore_launch(self, args: tuple[int, int]) -> None:
+        self.set_launch(*args)
 
     def launch_config(self) -> tuple[int, int]:
         a, b = C.c_int(), C.c_int()
@@ -137,7 +160,7 @@ class Engine:
     def upload_trace(self, packed, stream_row=None) -> DeviceTrace:
         torch = _torch()
         d = self.tdev
-        return DeviceTrace(
+        tr = DeviceTrace(
             slowdown=torch.from_numpy(np.ascontiguousarray(packed.slowdown)).to(d),
             n_segments=torch.from_numpy(packed.n_segments).to(d),
             seg_end=torch.from_numpy(packed.seg_end).to(d),
@@ -145,6 +168,9 @@ class Engine:
             seg_idle=torch.from_numpy(packed.seg_idle).to(d),
             stream_row=None if stream_row is None else torch.as_tensor(np.asarray(stream_row, np.int32)).to(d),
         )
+        if getattr(packed, "goal_n", None) is not None:
+            tr = tr.with_goal_changes(packed.goal_n, packed.goal_end, packed.goal_spec)
+        return tr
 
     def new_state(self, table: GpuTable, n: int, kalman=None, idle_cfg=None, stream=None) -> dict:
         torch = _torch()
@@ -200,14 +226,39 @@ class Engine:
                                    fb_latency.data_ptr(), fb_t_prof.data_ptr(), idle.data_ptr(),
                                    power_index.data_ptr(), n, self._stream(stream)))
 
-    def oracle_decide(self, table, specs, s, idle, plan_goal, *, stream_spec=None, stream=None):
+    def oracle_decide(self, table, specs, s, idle, plan_goal, *, stream_spec=None, stream=None, exact=False):
+        """Oracle decisions; with exact=True also the chosen configs' exact
+        predictions ([n, bytes] uint8 viewable as abi.PREDICTION_DTYPE)."""
         torch = _torch()
         specs = np.ascontiguousarray(specs, dtype=abi.SPEC_DTYPE)
         n = int(s.shape[0])
         out = torch.empty(n, dtype=torch.int32, device=self.tdev)
+        ex = torch.empty((n, abi.PREDICTION_DTYPE.itemsize), dtype=torch.uint8, device=self.tdev) if exact else None
         check(load().alert_oracle_decide(self.ctx, table.handle, specs.ctypes.data, len(specs),
                                          _ptr(stream_spec), s.data_ptr(), idle.data_ptr(), plan_goal.data_ptr(),
-                                         0, out.data_ptr(), n, self._stream(stream)))
+                                         0, out.data_ptr(), _ptr(ex), n, self._stream(stream)))
+        return (out, ex) if exact else out
+
+    def static_choice(self, table, specs, trace: DeviceTrace, state, *, stream_spec=None, stream_begin=0,
+                      stream_end=None, step_begin=0, step_end=None, stream=None):
+        """OracleStaticPolicy.begin for a range of streams (policy_aux <- cand | eligible << 16)."""
+        specs = np.ascontiguousarray(specs, dtype=abi.SPEC_DTYPE)
+        tr = trace.struct()
+        se = int(state["mu"].shape[0]) if stream_end is None else stream_end
+        te = trace.n_steps if step_end is None else step_end
+        check(load().alert_static_choice(self.ctx, table.handle, specs.ctypes.data, len(specs), _ptr(stream_spec),
+                                         C.byref(tr), state_struct(state), stream_begin, se, step_begin, te,
+                                         self._stream(stream)))
+
+    def baseline_decide(self, table, specs, state, plan_goal, *, policy, stream_spec=None, stream=None):
+        """One decide of a comparison scheme per stream (packed words, bits 0..17 and 30)."""
+        torch = _torch()
+        specs = np.ascontiguousarray(specs, dtype=abi.SPEC_DTYPE)
+        n = int(plan_goal.shape[0])
+        out = torch.empty(n, dtype=torch.int32, device=self.tdev)
+        check(load().alert_baseline_decide(self.ctx, table.handle, specs.ctypes.data, len(specs),
+                                           _ptr(stream_spec), state_struct(state), plan_goal.data_ptr(), policy,
+                                           out.data_ptr(), n, self._stream(stream)))
         return out
 
     def reduce(self, agg, stream=None):
@@ -254,4 +305,7 @@ def outputs_struct(records: dict | None = None, agg=None, forced=None, oracle_de
     if records and records.get("fb_latency") is not None:
         out.fb_latency = records["fb_latency"].data_ptr()
         out.fb_t_prof = records["fb_t_prof"].data_ptr()
+        for k in ("plan_goal", "phi"):
+            if records.get(k) is not None:
+                setattr(out, k, records[k].data_ptr())
     return out

@@ -21,7 +21,7 @@ from .estimator import (
 )
 from .model import DnnKind, kind_of
 from .packing import pack_specs
-from .records import decision_of
+from .records import decision_of, prediction_of
 
 POLICY_NAMES = ("alert", "alert-any", "alert-trad", "oracle", "oracle-static", "sys-only", "app-only",
                 "no-coord")
@@ -41,10 +41,27 @@ class GpuPolicy:
     def _finish(self, res) -> None:  # state after a fused run
         pass
 
+    def _prediction(self, cand: int, t_goal: float, spec_arr=None, acc_cand: int | None = None, **override):
+        """Prediction of one candidate at the current filter state
+        (alert_predict, predictor.py:147-197); ``override`` replaces fields
+        the way the comparison schemes build theirs (policies.py:314-428)."""
+        import torch
+
+        eng = self._engine()
+        g = torch.tensor([float(t_goal)], dtype=torch.float64, device=eng.tdev)
+        raw = eng.predict(self._table, self._specs if spec_arr is None else spec_arr, self._state, g)
+        preds = raw[0].cpu().numpy().view(abi.PREDICTION_DTYPE).reshape(-1)
+        p = dict(zip(preds.dtype.names, preds[cand].tolist()))
+        if acc_cand is not None:
+            p["expected_accuracy"] = float(preds[acc_cand]["expected_accuracy"])
+        p.update(override)
+        return prediction_of(self._table.candidates, cand, p)
+
 
 class AlertPolicy(GpuPolicy):
     """Coordinated selection from the shared slow-down / idle-power filters
-    (policies.py:70-108), evaluated on the GPU."""
+    (policies.py:70-108), evaluated on the GPU.  The DNN-kind filter comes
+    from ``kinds`` (policies.py:99-102) whatever the ``name`` label is."""
 
     def __init__(self, kalman: KalmanConfig | None = None, idle_cfg: IdleFilterConfig | None = None,
                  kinds: frozenset | None = None, name: str = "alert", device: int = 0):
@@ -52,7 +69,7 @@ class AlertPolicy(GpuPolicy):
         self.idle_cfg = idle_cfg
         self.kinds = kinds
         self.name = name
-        self.code_name = name
+        self.code_name = _kinds_code(kinds)
         self.device = device
 
     def begin(self, space, spec, env) -> None:
@@ -73,12 +90,14 @@ class AlertPolicy(GpuPolicy):
         import torch
 
         eng = self._engine()
+        self._specs = pack_specs([self.spec])  # policy.spec may be swapped between inputs (goal changes)
         self._goal.fill_(float(t_goal))
         code = {"alert": abi.POLICY_ALERT, "alert-any": abi.POLICY_ALERT_ANY,
-                "alert-trad": abi.POLICY_ALERT_TRAD}[self.name]
+                "alert-trad": abi.POLICY_ALERT_TRAD}[self.code_name]
         w = int(eng.decide(self._table, self._specs, self._state, self._goal, policy=code)[0].item())
         w &= 0xFFFFFFFF
-        return decision_of(self._table.candidates, w & 0xFFFF, (w >> 16) & 3)
+        c = w & 0xFFFF
+        return decision_of(self._table.candidates, c, (w >> 16) & 3, prediction=self._prediction(c, t_goal))
 
     def observe(self, record) -> None:
         import torch
@@ -139,10 +158,14 @@ class OraclePolicy(GpuPolicy):
 
     def decide(self, index: int, t_goal: float):
         eng = self._engine()
+        self._specs = pack_specs([self.spec])  # policy.spec may be swapped between inputs (goal changes)
         self._goal.fill_(float(t_goal))
-        w = int(eng.oracle_decide(self._table, self._specs, self._s[index:index + 1],
-                                  self._idle[index:index + 1], self._goal)[0].item()) & 0xFFFFFFFF
-        return decision_of(self._table.candidates, w & 0xFFFF, (w >> 16) & 3)
+        w, ex = eng.oracle_decide(self._table, self._specs, self._s[index:index + 1],
+                                  self._idle[index:index + 1], self._goal, exact=True)
+        w = int(w[0].item()) & 0xFFFFFFFF
+        c = w & 0xFFFF
+        p = ex[0].cpu().numpy().view(abi.PREDICTION_DTYPE)[0]
+        return decision_of(self._table.candidates, c, (w >> 16) & 3, prediction=prediction_of(self._table.candidates, c, p))
 
     def observe(self, record) -> None:
         pass
@@ -153,9 +176,11 @@ class BaselinePolicy(GpuPolicy):
     oracle-static (best fixed candidate over the realized trace), sys-only
     (fastest traditional DNN, cheapest on-time power cap), app-only (one
     anytime DNN at the maximum cap, best expected-accuracy stage), no-coord
-    (both controllers, uncoordinated).  They run through the fused path
-    (:func:`paper_1911_00119_b200.run` / ``run_batch``: one launch per
-    trace, FP64 with the reference's operation order)."""
+    (both controllers, uncoordinated).  Inside :func:`paper_1911_00119_b200.run`
+    / ``run_batch`` a whole trace runs in one launch (FP64, the reference's
+    operation order); driven step by step, ``begin`` / ``decide`` /
+    ``observe`` launch alert_static_choice / alert_baseline_decide /
+    alert_observe."""
 
     def __init__(self, name: str, kalman: KalmanConfig | None = None, device: int = 0):
         self.name = name
@@ -164,7 +189,10 @@ class BaselinePolicy(GpuPolicy):
         self.device = device
 
     def begin(self, space, spec, env) -> None:
-        from .packing import baseline_dnns
+        import torch
+
+        from .packing import baseline_dnns, policy_code
+        from .trace import pack_envs
 
         sys_dnn, app_dnn = baseline_dnns(space)
         if self.name == "sys-only" and sys_dnn < 0:
@@ -172,13 +200,81 @@ class BaselinePolicy(GpuPolicy):
         if self.name in ("app-only", "no-coord") and app_dnn < 0:
             raise ValueError("space has no anytime DNN")  # policies.py:327-328
         self.space, self.spec, self.env = space, spec, env
+        eng = self._engine()
+        self._code = policy_code(self.name)
+        self._table = eng.table(space)
+        self._specs = pack_specs([spec])
+        # sys-only / no-coord keep their own idle filter with the default config (policies.py:295, 388)
+        self._state = eng.new_state(self._table, 1, self.kalman, None)
+        self._goal = torch.empty(1, dtype=torch.float64, device=eng.tdev)
+        self._last_power = len(space.powers) - 1  # no-coord's initial power (policies.py:385)
+        if self.name == "oracle-static":  # OracleStaticPolicy.begin (policies.py:221-265)
+            tr = eng.upload_trace(pack_envs([env], dtype=np.float64))
+            eng.static_choice(self._table, self._specs, tr, self._state)
 
     def decide(self, index: int, t_goal: float):
-        raise NotImplementedError(f"{self.name}: the comparison schemes run fused over a whole trace "
-                                  "(paper_1911_00119_b200.run / run_batch), not step by step")
+        eng = self._engine()
+        self._goal.fill_(float(t_goal))
+        w = int(eng.baseline_decide(self._table, self._specs, self._state, self._goal,
+                                    policy=self._code)[0].item()) & 0xFFFFFFFF
+        c, feasible = w & 0xFFFF, bool((w >> 30) & 1)
+        cands = self._table.candidates
+        if self.name == "oracle-static":
+            pred = prediction_of(cands, c, {"latency_mean": 0.0, "latency_sigma": 0.0,
+                                            "pr_deadline": 1.0 if feasible else 0.0,
+                                            "expected_accuracy": 0.0, "energy": 0.0})
+        elif self.name == "sys-only":
+            sp = np.array(self._specs, copy=True)
+            sp["has_pr"] = 0  # predict_energy_mean (policies.py:309, 320)
+            acc = float(self.space.dnns[int(cands[c, 0])].stages[0].accuracy)
+            pred = self._prediction(c, t_goal, sp, pr_deadline=1.0 if feasible else 0.0, expected_accuracy=acc)
+        else:
+            acc_c = c
+            if self.name == "no-coord":  # expected accuracy at the previous power (policies.py:399-405)
+                i, _, st = (int(v) for v in cands[c])
+                acc_c = int(np.flatnonzero((cands[:, 0] == i) & (cands[:, 1] == self._last_power)
+                                           & (cands[:, 2] == st))[0])
+            pred = self._prediction(c, t_goal, acc_cand=acc_c, pr_deadline=0.0, energy=0.0)
+        self._last_power = int(cands[c, 1])
+        return decision_of(cands, c, 0, feasible, pred)
 
     def observe(self, record) -> None:
-        raise NotImplementedError(f"{self.name}: use paper_1911_00119_b200.run / run_batch")
+        import torch
+
+        if self.name == "oracle-static":  # policies.py:271-272
+            return
+        eng = self._engine()
+        d = eng.tdev
+        f64 = torch.float64
+        # app-only updates only the slow-down filter (policies.py:359-360); its
+        # idle estimate is never read, so updating it too changes nothing
+        eng.observe(self._table, self._state,
+                    torch.tensor([float(record.fb_latency)], dtype=f64, device=d),
+                    torch.tensor([float(record.fb_t_prof)], dtype=f64, device=d),
+                    torch.tensor([float(record.idle_power_true)], dtype=f64, device=d),
+                    torch.tensor([int(record.decision.power_index)], dtype=torch.int32, device=d),
+                    kalman=self.kalman)
+
+    def _finish(self, res) -> None:
+        import torch
+
+        for k, v in res.state.items():
+            if k in self._state:
+                self._state[k].copy_(torch.as_tensor(np.asarray(v)))
+
+
+def _kinds_code(kinds) -> str:
+    """Policy code of an AlertPolicy's DNN-kind filter (policies.py:99-102)."""
+    if kinds is None:
+        return "alert"
+    k = frozenset(kinds)
+    if k == frozenset({DnnKind.ANYTIME}):
+        return "alert-any"
+    if k == frozenset({DnnKind.TRADITIONAL}):
+        return "alert-trad"
+    if k == frozenset({DnnKind.ANYTIME, DnnKind.TRADITIONAL}):
+        return "alert"
+    raise ValueError(f"unsupported DNN kinds filter {set(kinds)}")
 
 
 def make_policy(name: str, kalman: KalmanConfig | None = None, device: int = 0):

@@ -103,9 +103,22 @@ class RunResult:  # simulator.py:422-425
     summary: Summary
 
 
-def decision_of(cands: np.ndarray, cand: int, level: int) -> ConfigDecision:
+def decision_of(cands: np.ndarray, cand: int, level: int, feasible: bool | None = None,
+                prediction: Prediction | None = None) -> ConfigDecision:
+    """ConfigDecision of candidate ``cand``; ``feasible`` defaults to level
+    NONE (selector.py:126), the comparison schemes pass their own
+    (policies.py:266-271, 305-310)."""
     i, j, st = (int(v) for v in cands[cand])
-    return ConfigDecision(i, j, st if st else None, None, level == 0, LEVELS[level])
+    return ConfigDecision(i, j, st if st else None, prediction, level == 0 if feasible is None else bool(feasible),
+                          LEVELS[level])
+
+
+def prediction_of(cands: np.ndarray, cand: int, p) -> Prediction:
+    """Prediction of candidate ``cand`` from an AlertPrediction-like record
+    (fields latency_mean, latency_sigma, pr_deadline, expected_accuracy, energy)."""
+    i, j, st = (int(v) for v in cands[cand])
+    return Prediction(i, j, st if st else None, float(p["latency_mean"]), float(p["latency_sigma"]),
+                      float(p["pr_deadline"]), float(p["expected_accuracy"]), float(p["energy"]))
 
 
 def summary_from_agg(agg: np.ndarray, n_phases: int = abi.MAX_PHASES) -> Summary:

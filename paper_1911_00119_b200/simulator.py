@@ -20,9 +20,9 @@ from . import abi
 from .engine import DeviceTrace, Engine, GpuTable, outputs_struct
 from .packing import mode_runs, pack_specs, policy_code
 from .records import (
-    RunResult, StepRecord, Summary, ViolationFlags, decision_of, summary_from_agg,
+    RunResult, StepRecord, Summary, ViolationFlags, decision_of, prediction_of, summary_from_agg,
 )
-from .trace import PackedEnvs, TrueEnvironment, pack_envs, realize
+from .trace import PackedEnvs, TrueEnvironment, pack_envs, pack_goal_changes, realize
 
 _ENGINES: dict[int, Engine] = {}
 
@@ -64,8 +64,9 @@ def _as_device_trace(engine: Engine, envs, trace_dtype, stream_row) -> DeviceTra
 def run_batch(space, specs: Sequence, envs, policy: str = "alert", *, kalman=None, idle_cfg=None,
               group_sizes=None, stream_spec=None, stream_row=None, n_streams: int | None = None,
               records: str | None = None, forced=None, flags: int = 0, chunk_steps: int | None = None,
-              trace_dtype=np.float32, engine: Engine | None = None, device: int = 0,
-              keep_on_device: bool = False, lanes_per_stream: int | None = None) -> BatchResult:
+              trace_dtype=np.float64, engine: Engine | None = None, device: int = 0,
+              keep_on_device: bool = False, lanes_per_stream: int | None = None,
+              goal_changes=None) -> BatchResult:
     """Run ``policy`` over many independent streams in one fused launch.
 
     specs        ConstraintSpec objects (or an AlertSpec record array); stream k
@@ -75,23 +76,57 @@ def run_batch(space, specs: Sequence, envs, policy: str = "alert", *, kalman=Non
     records      None (aggregates only), "f32" or "f64" per-step records.
     forced       [n_steps, n_streams] int32 candidate indices to execute
                  (teacher forcing; -1 = own decision).
+    trace_dtype  slow-down dtype when ``envs`` are packed here: float64 keeps
+                 the reference's values (default); float32 halves the trace
+                 bytes (the decisions then follow the FP32-rounded inputs).
+    goal_changes per trace row None or [(start_step, spec_index), ...] from
+                 step 0 (trace.pack_goal_changes): the row's constraint spec
+                 changes at those inputs (overrides stream_spec).
+    lanes_per_stream  tile width for this call only (the engine's launch
+                 settings are restored afterwards).
     """
     torch = __import__("torch")
     eng = engine or get_engine(device)
+    prev_launch = None
     if lanes_per_stream is not None:
-        eng.set_launch(lanes_per_stream, 0)
+        prev_launch = eng.set_launch(lanes_per_stream, 0)
+    try:
+        return _run_batch(eng, torch, space, specs, envs, policy, kalman, idle_cfg, group_sizes, stream_spec,
+                          stream_row, n_streams, records, forced, flags, chunk_steps, trace_dtype,
+                          keep_on_device, goal_changes)
+    finally:
+        if prev_launch is not None:
+            eng.restore_launch(prev_launch)
+
+
+def _run_batch(eng, torch, space, specs, envs, policy, kalman, idle_cfg, group_sizes, stream_spec, stream_row,
+               n_streams, records, forced, flags, chunk_steps, trace_dtype, keep_on_device, goal_changes):
     table: GpuTable = eng.table(space)
     spec_arr = specs if isinstance(specs, np.ndarray) and specs.dtype == abi.SPEC_DTYPE \
         else pack_specs(list(specs), group_sizes)
     trace = _as_device_trace(eng, envs, trace_dtype, stream_row)
+    if goal_changes is not None:
+        if isinstance(goal_changes, tuple) and len(goal_changes) == 3 and isinstance(goal_changes[0], np.ndarray):
+            gn, ge, gs = goal_changes
+        else:
+            gn, ge, gs = pack_goal_changes(goal_changes, trace.n_steps, len(spec_arr))
+        if len(gn) != trace.n_rows:
+            raise ValueError(f"goal_changes has {len(gn)} rows, the trace {trace.n_rows}")
+        trace = trace.with_goal_changes(gn, ge, gs)
+        stream_spec_mode_split = False
+    else:
+        stream_spec_mode_split = trace.goal_n is None
     if stream_row is not None and trace.stream_row is None:
         trace.stream_row = torch.as_tensor(np.asarray(stream_row, np.int32)).to(eng.tdev)
     ns = n_streams if n_streams is not None else (
         len(stream_row) if stream_row is not None else trace.n_rows)
     steps = trace.n_steps
     dev = eng.tdev
-    # launches: one per contiguous run of streams with one goal mode
-    if stream_spec is not None:
+    # launches: one per contiguous run of streams with one goal mode (a
+    # trace with goal changes runs as one launch over every spec)
+    if stream_spec is not None and not stream_spec_mode_split:
+        launches = [(0, None, spec_arr, torch.as_tensor(np.asarray(stream_spec, np.int32)).to(dev))]
+    elif stream_spec is not None:
         launches = [(b, e, sp, torch.as_tensor(full).to(dev)) for b, e, sp, full in mode_runs(spec_arr, stream_spec)]
     else:
         launches = [(0, None, spec_arr, None)]
@@ -103,8 +138,8 @@ def run_batch(space, specs: Sequence, envs, policy: str = "alert", *, kalman=Non
         rec["decision"] = torch.empty((steps, ns), dtype=torch.int32, device=dev)
         for k in ("energy", "accuracy", "latency", "mu", "sigma2"):
             rec[k] = torch.empty((steps, ns), dtype=vdt, device=dev)
-        if records == "f64":  # StepRecord feedback pair (fb_latency, fb_t_prof)
-            for k in ("fb_latency", "fb_t_prof"):
+        if records == "f64":  # StepRecord feedback pair (fb_latency, fb_t_prof), plan goal, phi
+            for k in ("fb_latency", "fb_t_prof", "plan_goal", "phi"):
                 rec[k] = torch.empty((steps, ns), dtype=torch.float64, device=dev)
     pol = policy_code(policy)
     od = None
@@ -218,28 +253,50 @@ class HostStreamer:
         return self.agg_host
 
 
-def run(space, spec, trace, policy) -> RunResult:
+def run(space, spec, trace, policy, goal_changes=None) -> RunResult:
     """Drop-in for simulator.run (simulator.py:461-507) with a policy from
     :func:`make_policy`: realize the trace (same numpy draws as the
-    reference), then one fused GPU launch over all inputs.  Records carry
-    FP64 values; ``decision.prediction`` is not materialised (None)."""
+    reference), then one fused GPU launch over all inputs.  Records carry the
+    reference's fields in FP64: ``period`` = plan goal + overhead
+    (simulator.py:483), ``decision.feasible`` and ``decision.prediction`` as
+    the reference's policies set them (selector.py:122-128, policies.py:201-205,
+    266-271, 305-320, 357-368, 417-428), the latter from one batched
+    ``alert_predict`` launch over the per-step filter states.
+
+    goal_changes  optional [(input_index, ConstraintSpec), ...]: from that
+                  input on the run is measured against, and the policy plans
+                  for, the new spec (the reference's ``policy.spec`` swapped
+                  between inputs; SURVEY §7 hard part 8).
+    """
     from .policies import GpuPolicy
 
     if not isinstance(policy, GpuPolicy):
         raise TypeError("run() executes the policies of paper_1911_00119_b200.make_policy on the GPU; "
                         f"got {type(policy).__name__}")
     env = realize(trace)
+    specs = [spec] + [c for _, c in (goal_changes or ())]
+    sched = None
+    if goal_changes:
+        sched = [[(0, 0)] + [(int(n), k + 1) for k, (n, _) in enumerate(goal_changes)]]
     policy.begin(space, spec, env)
-    res = run_batch(space, [spec], [env], policy.code_name, kalman=policy.kalman,
-                    idle_cfg=getattr(policy, "idle_cfg", None), group_sizes=trace.group_size,
-                    records="f64", trace_dtype=np.float64, device=policy.device)
+    spec_arr = pack_specs(specs, trace.group_size)
+    res = run_batch(space, spec_arr, [env], policy.code_name, kalman=policy.kalman,
+                    idle_cfg=getattr(policy, "idle_cfg", None), records="f64", trace_dtype=np.float64,
+                    device=policy.device, goal_changes=sched, stream_spec=[0])
     policy._finish(res)
+    n_in = len(env.slowdown)
+    spec_idx = np.zeros(n_in, np.int32)
+    for k, (start, _) in enumerate(goal_changes or ()):
+        spec_idx[int(start):] = k + 1
+    preds = chosen_predictions(policy._engine(), space, spec_arr, policy.code_name, res, spec_idx,
+                               kalman=policy.kalman, idle_cfg=getattr(policy, "idle_cfg", None))
     d = res.decoded()
     cands = res.candidates
+    oh = [float(sp.overhead_budget) for sp in specs]
     recs = []
-    for n in range(len(env.slowdown)):
+    for n in range(n_in):
         c = int(d["cand"][n, 0])
-        dec = decision_of(cands, c, int(d["level"][n, 0]))
+        dec = decision_of(cands, c, int(d["level"][n, 0]), bool(d["feasible"][n, 0]), preds[n])
         recs.append(StepRecord(
             input_index=n, decision=dec, true_slowdown=float(env.slowdown[n]),
             observed_latency=float(res.records["latency"][n, 0]), completed_stage=int(d["completed"][n, 0]),
@@ -247,10 +304,94 @@ def run(space, spec, trace, policy) -> RunResult:
             energy=float(res.records["energy"][n, 0]),
             violations=ViolationFlags(bool(d["viol_lat"][n, 0]), bool(d["viol_acc"][n, 0]),
                                       bool(d["viol_energy"][n, 0])),
-            phase_index=int(env.phase_index[n]), idle_power_true=float(env.idle_power[n]),
+            phase_index=int(env.phase_index[n]),
+            period=float(res.records["plan_goal"][n, 0]) + oh[spec_idx[n]],
             fb_latency=float(res.records["fb_latency"][n, 0]), fb_t_prof=float(res.records["fb_t_prof"][n, 0]),
+            idle_power_true=float(env.idle_power[n]),
         ))
     return RunResult(tuple(recs), summary_from_agg(res.agg[0], len(trace.phases)))
+
+
+def chosen_predictions(eng: Engine, space, spec_arr: np.ndarray, policy: str, res: BatchResult,
+                       spec_idx: np.ndarray, stream: int = 0, kalman=None, idle_cfg=None,
+                       chunk: int = 4096) -> list:
+    """``ConfigDecision.prediction`` of every step of one stream of an f64
+    run_batch result, as the reference's policies build it:
+
+    * alert / alert-any / alert-trad: the chosen entry of predict_all at the
+      state the decide saw (selector.py:122-128) — one alert_predict launch
+      per chunk of steps, each step a "stream" whose state is the previous
+      step's (mu, sigma2, phi) record (the initial state for step 0);
+    * oracle: _exact_pred of the executed config (policies.py:201-205): the
+      step's measured latency / met / accuracy / energy;
+    * oracle-static: _exact_pred(.., eligible, 0, 0, 0) (policies.py:266-271);
+    * sys-only: mean-energy prediction, pr 1/0 by feasibility (policies.py:314-320);
+    * app-only / no-coord: latency from the estimator, the best stage's
+      expected accuracy (no-coord: at the previous power), pr 0, energy 0
+      (policies.py:357-368, 417-428)."""
+    torch = __import__("torch")
+    from .records import Prediction
+
+    rec = res.records
+    n = rec["decision"].shape[0]
+    d = abi.decode_decision(np.asarray(rec["decision"])[:, stream].view(np.uint32))
+    cand, feas = d["cand"], d["feasible"]
+    cands = res.candidates
+    if policy == "oracle":
+        return [prediction_of(cands, int(cand[k]), {
+            "latency_mean": rec["latency"][k, stream], "latency_sigma": 0.0,
+            "pr_deadline": 1.0 if d["met"][k] else 0.0, "expected_accuracy": rec["accuracy"][k, stream],
+            "energy": rec["energy"][k, stream]}) for k in range(n)]
+    if policy == "oracle-static":
+        return [prediction_of(cands, int(cand[k]), {
+            "latency_mean": 0.0, "latency_sigma": 0.0, "pr_deadline": 1.0 if feas[k] else 0.0,
+            "expected_accuracy": 0.0, "energy": 0.0}) for k in range(n)]
+    table = eng.table(space)
+    sp = np.array(spec_arr, copy=True)
+    if policy == "sys-only":
+        sp["has_pr"] = 0  # predict_energy_mean (policies.py:309, 320)
+    init = eng.new_state(table, 1, kalman, idle_cfg)
+    st0 = {k: float(init[k][0].item()) for k in ("mu", "sigma2", "phi")}
+    prev = {k: np.concatenate([[st0[k]], np.asarray(rec[k])[:-1, stream]]) for k in ("mu", "sigma2", "phi")}
+    goal = np.asarray(rec["plan_goal"])[:, stream]
+    # the candidate whose prediction is reported (no-coord: accuracy at the previous power)
+    pick = cand.astype(np.int64)
+    acc_pick = pick
+    if policy == "no-coord":
+        power = cands[cand, 1]
+        old = np.concatenate([[len(space.powers) - 1], power[:-1]])
+        index = {tuple(c): k for k, c in enumerate(cands.tolist())}
+        acc_pick = np.array([index[(int(cands[c, 0]), int(o), int(cands[c, 2]))] for c, o in zip(cand, old)])
+    pv = np.zeros(n, abi.PREDICTION_DTYPE)
+    pa = np.zeros(n, abi.PREDICTION_DTYPE)
+    for b in range(0, n, chunk):
+        e = min(n, b + chunk)
+        st = eng.new_state(table, e - b, kalman, idle_cfg)
+        for k in ("mu", "sigma2", "phi"):
+            st[k].copy_(torch.from_numpy(np.ascontiguousarray(prev[k][b:e])))
+        g = torch.from_numpy(np.ascontiguousarray(goal[b:e])).to(eng.tdev)
+        ss = torch.from_numpy(np.ascontiguousarray(spec_idx[b:e], np.int32)).to(eng.tdev)
+        raw = eng.predict(table, sp, st, g, stream_spec=ss)  # [e - b, C, bytes]
+        rows = torch.arange(e - b, device=eng.tdev)
+        for dst, idx in ((pv, pick), (pa, acc_pick)):
+            sel = raw[rows, torch.from_numpy(idx[b:e]).to(eng.tdev)]
+            dst[b:e] = sel.cpu().numpy().view(abi.PREDICTION_DTYPE).reshape(-1)
+    out = []
+    for k in range(n):
+        c = int(cand[k])
+        if policy in ("alert", "alert-any", "alert-trad"):
+            out.append(prediction_of(cands, c, pv[k]))
+        elif policy == "sys-only":
+            i = int(cands[c, 0])
+            acc = float(space.dnns[i].stages[0].accuracy)
+            p = dict(zip(pv.dtype.names, pv[k].tolist()))
+            p.update(pr_deadline=1.0 if feas[k] else 0.0, expected_accuracy=acc)
+            out.append(prediction_of(cands, c, p))
+        else:  # app-only / no-coord
+            p = dict(zip(pv.dtype.names, pv[k].tolist()))
+            p.update(pr_deadline=0.0, expected_accuracy=float(pa[k]["expected_accuracy"]), energy=0.0)
+            out.append(prediction_of(cands, c, p))
+    return out
 
 
 def run_injected(space, spec, env: TrueEnvironment, policy: str = "alert", *, kalman=None,

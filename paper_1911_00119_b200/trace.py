@@ -20,6 +20,8 @@ from typing import Sequence, Union
 
 import numpy as np
 
+from . import abi
+
 MIN_SLOWDOWN = 0.01  # simulator.py:28
 
 
@@ -141,6 +143,10 @@ class PackedEnvs:
     seg_end: np.ndarray     # [n_rows, max_seg] int32
     seg_phase: np.ndarray   # [n_rows, max_seg] int32
     seg_idle: np.ndarray    # [n_rows, max_seg] float64
+    # goal changes (optional): per-row spec segments, see pack_goal_changes
+    goal_n: np.ndarray | None = None     # [n_rows] int32 (0 = the stream's own spec)
+    goal_end: np.ndarray | None = None   # [n_rows, max_goal] int32 exclusive end step
+    goal_spec: np.ndarray | None = None  # [n_rows, max_goal] int32 index into the spec array
 
     @property
     def n_rows(self) -> int:
@@ -188,10 +194,63 @@ def pack_envs(envs: Sequence, dtype=np.float32, max_segments: int | None = None)
     for r, sg in enumerate(segs):
         if len(sg) > ms:
             raise ValueError(f"environment {r} has {len(sg)} segments > {ms}")
+        bad = [ph for _, ph, _ in sg if not 0 <= ph < abi.MAX_PHASES]
+        if bad:  # per-phase sums exist for phase ids < MAX_PHASES only (ALERT_AGG_PHASE_*)
+            raise ValueError(f"environment {r}: phase index {bad[0]} outside 0..{abi.MAX_PHASES - 1}; "
+                             f"traces with more than {abi.MAX_PHASES} phases are not supported")
         n_seg[r] = len(sg)
         for k, (end, ph, idle) in enumerate(sg):
             seg_end[r, k], seg_phase[r, k], seg_idle[r, k] = end, ph, idle
     return PackedEnvs(slow, n_seg, seg_end, seg_phase, seg_idle)
+
+
+def pack_goal_changes(changes: Sequence, n_steps: int, n_specs: int):
+    """Goal changes per trace row -> (goal_n, goal_end, goal_spec) arrays
+    (AlertTrace.goal_*).  ``changes[r]`` is None (the stream's own spec) or a
+    sequence of (start_step, spec_index) pairs with strictly increasing starts,
+    the first at step 0: from start_step on, the row runs under
+    specs[spec_index] (the reference's policy.spec swapped at that input,
+    SURVEY §7 hard part 8)."""
+    rows = len(changes)
+    segs = []
+    for r, ch in enumerate(changes):
+        if ch is None or len(ch) == 0:
+            segs.append([])
+            continue
+        ch = [(int(a), int(b)) for a, b in ch]
+        if ch[0][0] != 0:
+            raise ValueError(f"goal changes of row {r} must start at step 0")
+        for (a, _), (b, _) in zip(ch, ch[1:]):
+            if not a < b:
+                raise ValueError(f"goal changes of row {r} must have increasing steps")
+        if ch[-1][0] >= n_steps:
+            raise ValueError(f"goal change of row {r} at step {ch[-1][0]} is past the trace ({n_steps} steps)")
+        for _, k in ch:
+            if not 0 <= k < n_specs:
+                raise ValueError(f"goal change of row {r}: spec index {k} outside 0..{n_specs - 1}")
+        segs.append([(ch[i + 1][0] if i + 1 < len(ch) else n_steps, k) for i, (_, k) in enumerate(ch)])
+    mg = max(1, max(len(s) for s in segs))
+    goal_n = np.zeros(rows, np.int32)
+    goal_end = np.zeros((rows, mg), np.int32)
+    goal_spec = np.zeros((rows, mg), np.int32)
+    for r, sg in enumerate(segs):
+        goal_n[r] = len(sg)
+        for k, (end, si) in enumerate(sg):
+            goal_end[r, k], goal_spec[r, k] = end, si
+    return goal_n, goal_end, goal_spec
+
+
+def goal_index_per_step(goal_n, goal_end, goal_spec, row: int, n_steps: int, default: int) -> np.ndarray:
+    """Spec index in force at every step of one row (host view of the goal arrays)."""
+    out = np.full(n_steps, default, np.int32)
+    if goal_n is None or goal_n[row] == 0:
+        return out
+    start = 0
+    for k in range(int(goal_n[row])):
+        end = int(goal_end[row, k])
+        out[start:end] = goal_spec[row, k]
+        start = end
+    return out
 
 
 def unpack_row(p: PackedEnvs, row: int) -> TrueEnvironment:

@@ -26,6 +26,12 @@ def golden_predict():
 
 
 @pytest.fixture(scope="session")
+def golden_goals():
+    from helpers import load_golden_runs
+    return load_golden_runs("golden_goals.npz")
+
+
+@pytest.fixture(scope="session")
 def golden_baselines():
     from helpers import load_golden_runs
     return load_golden_runs("golden_baselines.npz")

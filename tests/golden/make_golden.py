@@ -89,6 +89,10 @@ def run_case(space, spec, trace, policy_name, kalman=None, env=None):
         res = run(space, spec, trace, pol)
     finally:
         S.realize = orig
+    return _records_out(space, res, pol, env)
+
+
+def _records_out(space, res, pol, env):
     recs = res.records
     out = {
         "cand": np.array([cand_index(space, r.decision.dnn_index, r.decision.power_index,
@@ -100,6 +104,11 @@ def run_case(space, spec, trace, policy_name, kalman=None, env=None):
         "viol": np.array([(r.violations.latency, r.violations.accuracy, r.violations.energy) for r in recs],
                          np.int32),
         "period": np.array([r.period for r in recs]),
+        "feasible": np.array([r.decision.feasible for r in recs], np.int32),
+        # ConfigDecision.prediction (selector.py:122-128 / policies.py:201-428)
+        "pred": np.array([(r.decision.prediction.latency_mean, r.decision.prediction.latency_sigma,
+                           r.decision.prediction.pr_deadline, r.decision.prediction.expected_accuracy,
+                           r.decision.prediction.energy) for r in recs]),
         "latency": np.array([r.observed_latency for r in recs]),
         "accuracy": np.array([r.delivered_accuracy for r in recs]),
         "energy": np.array([r.energy for r in recs]),
@@ -116,6 +125,133 @@ def run_case(space, spec, trace, policy_name, kalman=None, env=None):
                                    for p in res.summary.per_phase]),
     }
     return out
+
+
+def run_with_goal_changes(space, spec, trace, policy, changes, kalman=None, env=None):
+    """simulator.run (simulator.py:461-507) with goal changes mirrored as
+    SURVEY §7 hard part 8 prescribes: at input n >= change step the loop's
+    spec is replaced, policy.spec is swapped before decide (read there,
+    policies.py:97-103 / 160-205), plan_goal is recomputed from the new spec
+    exactly as simulator.py:473-483 does, and the input is measured against
+    it.  Everything else is the reference's own code, called unchanged."""
+    from alertsim.selector import GroupState, InfeasibleDeadlineError, adjust_goal
+    from alertsim.simulator import RunResult, _summarize, execute_decision, measure
+
+    env = env if env is not None else realize(trace)
+    policy.begin(space, spec, env)
+    records = []
+    group = None
+    cur = spec
+    pending = sorted(changes, key=lambda c: c[0])
+    for n in range(trace.length):
+        while pending and pending[0][0] <= n:
+            cur = pending.pop(0)[1]
+            policy.spec = cur
+        if trace.group_size is not None:
+            if group is None or group.remaining_count == 0:
+                group = GroupState(remaining_budget=trace.group_size * cur.t_goal,
+                                   remaining_count=trace.group_size)
+        try:
+            plan_goal = adjust_goal(cur, group)
+        except InfeasibleDeadlineError:
+            plan_goal = 0.001
+        period = plan_goal + cur.overhead_budget
+        decision = policy.decide(n, plan_goal)
+        s = float(env.slowdown[n])
+        outcome = execute_decision(s, decision, space, plan_goal)
+        record = measure(decision, outcome, cur, float(env.idle_power[n]), space, input_index=n,
+                         phase_index=int(env.phase_index[n]), period=period)
+        records.append(record)
+        policy.observe(record)
+        if group is not None:
+            group.remaining_budget -= record.observed_latency
+            group.remaining_count -= 1
+    return RunResult(records=tuple(records), summary=_summarize(records, len(trace.phases)))
+
+
+def goal_changes():
+    """Golden runs with goal changes (north_star "goal changes" as a trace
+    input; SURVEY §7 hard part 8): specs swap mid-trace, including mode flips,
+    group budgets and pr_threshold toggles, for every policy."""
+    space = preset_space()
+    ref = reference_latency(space)
+    oh = 0.01 * ref
+    e_min = ConstraintSpec(mode=Mode.MINIMIZE_ENERGY, t_goal=0.14, q_goal=0.68, overhead_budget=oh)
+    e_tight = ConstraintSpec(mode=Mode.MINIMIZE_ENERGY, t_goal=0.6 * ref, q_goal=0.85, overhead_budget=oh)
+    a_pr = ConstraintSpec(mode=Mode.MAXIMIZE_ACCURACY, t_goal=0.8 * ref, e_goal=0.6 * 50.0 * 0.8 * ref,
+                          pr_threshold=0.95, overhead_budget=oh)
+    a_loose = ConstraintSpec(mode=Mode.MAXIMIZE_ACCURACY, t_goal=1.5 * ref, e_goal=0.4 * 50.0 * 1.5 * ref,
+                             overhead_budget=oh)
+    cases = []
+    tr = preset_trace(phase_length=100)
+    sched_a = [(60, e_tight), (140, a_pr), (220, e_min)]        # mode flips
+    sched_b = [(1, a_loose), (150, a_pr), (151, e_tight), (299, e_min)]  # adjacent changes, last input
+    for pol in ("alert", "alert-any", "alert-trad", "oracle", "oracle-static", "sys-only", "app-only", "no-coord"):
+        cases.append((f"flip_{pol}", space, e_min, tr, pol, None, sched_a))
+    cases.append(("adjacent_alert", space, a_pr, tr, "alert", None, sched_b))
+    cases.append(("adjacent_oracle", space, a_pr, tr, "oracle", None, sched_b))
+    trg = replace(preset_trace(phase_length=40), group_size=4)
+    cases.append(("group4_alert", space, e_min, trg, "alert", None, [(37, e_tight), (90, a_pr)]))
+    cases.append(("group4_no-coord", space, e_min, trg, "no-coord", None, [(37, e_tight), (90, a_pr)]))
+    big = generate_space(ProfileKnobs(n_dnns=64, n_powers=32))
+    bref = reference_latency(big)
+    bmin = ConstraintSpec(mode=Mode.MINIMIZE_ENERGY, t_goal=1.0 * bref, q_goal=0.8, overhead_budget=0.01 * bref)
+    bacc = ConstraintSpec(mode=Mode.MAXIMIZE_ACCURACY, t_goal=0.8 * bref, e_goal=0.6 * 50.0 * 0.8 * bref,
+                          overhead_budget=0.01 * bref)
+    btr = preset_trace(phase_length=20)
+    cases.append(("big64x32_alert", big, bmin, btr, "alert", None, [(25, bacc), (41, bmin)]))
+    rnd = random.Random(4242)
+    for k in range(12):
+        rs = random_space(rnd)
+        specs = [random_spec(rnd) for _ in range(3)]
+        specs = [replace(sp, overhead_budget=rnd.choice([0.0, 0.01 * sp.t_goal])) for sp in specs]
+        trr = random_trace(rnd, 80)
+        pol = ["alert", "oracle", "alert-any", "sys-only"][k % 4]
+        if pol == "alert-any" and not any(d.kind is DnnKind.ANYTIME for d in rs.dnns):
+            pol = "alert"
+        if pol == "sys-only" and not any(d.kind is DnnKind.TRADITIONAL for d in rs.dnns):
+            pol = "alert"
+        steps = sorted(rnd.sample(range(1, 80), 2))
+        cases.append((f"random{k:02d}_{pol}", rs, specs[0], trr, pol, None,
+                      [(steps[0], specs[1]), (steps[1], specs[2])]))
+    arrays, meta = {}, []
+    for name, sp, spec, tr_, pol, kal, sched in cases:
+        env = realize(tr_)
+        pobj = Recording(make_policy(pol, kalman=kal))
+        # Recording forwards spec swaps to the wrapped policy
+        res = run_with_goal_changes(sp, spec, tr_, _SpecForward(pobj), sched, env=env)
+        out = _records_out(sp, res, pobj, env)
+        for key, val in out.items():
+            arrays[f"{name}/{key}"] = val
+        meta.append({"name": name, "space": space_to_dict(sp), "spec": spec_json(spec, tr_.group_size),
+                     "changes": [[int(n), spec_json(c, tr_.group_size)] for n, c in sched],
+                     "policy": pol, "kalman": kalman_json(kal), "n_phases": len(tr_.phases)})
+        print(name, "E", out["summary"][0], "acc", out["summary"][1])
+    arrays["meta"] = np.frombuffer(json.dumps(meta).encode(), np.uint8)
+    np.savez_compressed(OUT / "golden_goals.npz", **arrays)
+
+
+class _SpecForward:
+    """Policy wrapper whose ``spec`` assignments reach the wrapped reference policy."""
+
+    def __init__(self, rec):
+        self.rec = rec
+        self.name = rec.name
+
+    def __setattr__(self, key, value):
+        if key == "spec":
+            self.rec.inner.spec = value
+        else:
+            object.__setattr__(self, key, value)
+
+    def begin(self, space, spec, env):
+        self.rec.begin(space, spec, env)
+
+    def decide(self, index, t_goal):
+        return self.rec.decide(index, t_goal)
+
+    def observe(self, record):
+        self.rec.observe(record)
 
 
 def spec_json(spec, group_size=None):
@@ -328,6 +464,8 @@ def sweeps():
 if __name__ == "__main__":
     if "--sweeps" in sys.argv:
         sweeps()
+    elif "--goals" in sys.argv:
+        goal_changes()
     elif "--baselines" in sys.argv:
         baselines()
     else:

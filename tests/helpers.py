@@ -47,6 +47,8 @@ class GoldenCase:
         self.policy = meta["policy"]
         self.kalman = kalman_from_json(meta["kalman"])
         self.n_phases = meta["n_phases"]
+        # goal changes (golden_goals.npz): [(input_index, ConstraintSpec), ...]
+        self.changes = [(int(n), spec_from_json(d)) for n, d in meta.get("changes", [])] or None
         self.z = {k.split("/", 1)[1]: z[k] for k in z.files if k.startswith(self.name + "/")}
 
     @property

@@ -39,8 +39,8 @@ def test_abi_struct_sizes_match_header():
     assert C.sizeof(abi.AlertSpec) == 64
     assert C.sizeof(abi.AlertFilterConfig) == 80
     assert C.sizeof(abi.AlertPrediction) == 56
-    assert C.sizeof(abi.AlertOutputs) == 8 * 7 + 8 + 8 * 4 + 8 * 2
-    assert C.sizeof(abi.AlertTrace) == 8 + 8 + 8 * 4 + 8 + 8 * 5
+    assert C.sizeof(abi.AlertOutputs) == 8 * 7 + 8 + 8 * 4 + 8 * 4
+    assert C.sizeof(abi.AlertTrace) == 8 + 8 + 8 * 4 + 8 + 8 * 5 + 8 + 8 * 3
     assert C.sizeof(abi.AlertSpaceDesc) == 8 + 8 * 6 + 8 + 8
     assert C.sizeof(abi.AlertState) == 8 * 10
 
@@ -49,7 +49,7 @@ def test_version_and_strerror():
     from paper_1911_00119_b200 import _lib
 
     L = _lib.load()
-    assert L.alert_abi_version() == 2
+    assert L.alert_abi_version() == 3
     assert L.alert_strerror(-3) == b"invalid constraint spec"
 
 

@@ -29,8 +29,12 @@ def check_golden(case):
     """The oracle reproduces one reference run bit for bit."""
     if True:
         rec, agg, st = oracle.run(case.space, case.spec, case.env, case.policy, kalman=case.kalman,
-                                  group_size=case.group_size)
+                                  group_size=case.group_size, goal_changes=case.changes)
         z = case.z
+        np.testing.assert_array_equal(rec["feasible"], z["feasible"], err_msg=case.name)
+        ours = np.stack([rec[f] for f in ("pred_latency_mean", "pred_latency_sigma", "pred_pr", "pred_accuracy",
+                                          "pred_energy")], 1)
+        np.testing.assert_array_equal(ours, z["pred"], err_msg=f"{case.name}:prediction")
         np.testing.assert_array_equal(rec["cand"], z["cand"], err_msg=case.name)
         np.testing.assert_array_equal(rec["level"], z["level"], err_msg=case.name)
         np.testing.assert_array_equal(rec["completed"], z["completed"], err_msg=case.name)
@@ -75,6 +79,23 @@ def test_golden_baselines_bit_exact(golden_baselines):
     assert {c.policy for c in golden_baselines} == {"oracle-static", "sys-only", "app-only", "no-coord"}
     for case in golden_baselines:
         check_golden(case)
+
+
+def test_golden_goal_changes_bit_exact(golden_goals):
+    """Goal changes mid-trace (north_star "goal changes"; the reference's run
+    loop with policy.spec swapped, tests/golden/make_golden.py
+    run_with_goal_changes): every policy, mode flips, groups, adjacent
+    changes, the 64x32 table and random spaces."""
+    assert len(golden_goals) >= 20
+    assert {c.policy for c in golden_goals} >= {"alert", "alert-any", "alert-trad", "oracle", "oracle-static",
+                                               "sys-only", "app-only", "no-coord"}
+    flips = 0
+    for case in golden_goals:
+        assert case.changes
+        check_golden(case)
+        modes = {case.spec.mode} | {c.mode for _, c in case.changes}
+        flips += len(modes) > 1
+    assert flips >= 8
 
 
 def test_published_acceptance_numbers(golden_runs):
