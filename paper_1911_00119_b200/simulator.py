@@ -178,11 +178,13 @@ class HostStreamer:
     copied host->device on a copy stream while the kernel runs chunk i on the
     compute stream (double buffer, CUDA events), with the filter state and
     aggregates carried on the device between chunks (alert_run step ranges).
+    The scenario map (stream_spec, and stream_row when scenarios share trace
+    rows) is copied from pinned host memory at the start of every pass.
     This is the end-to-end path: inputs from host, per-stream summaries back.
     """
 
     def __init__(self, space, specs, packed: PackedEnvs, policy: str = "alert", *, kalman=None,
-                 idle_cfg=None, group_sizes=None, stream_spec=None, chunk_steps: int = 1000,
+                 idle_cfg=None, group_sizes=None, stream_spec=None, stream_row=None, chunk_steps: int = 1000,
                  engine: Engine | None = None, device: int = 0):
         torch = __import__("torch")
         self.torch = torch
@@ -195,21 +197,40 @@ class HostStreamer:
             raise ValueError("oracle-static is clairvoyant over the whole trace: use run_batch (device-resident "
                              "trace), not the chunked host streamer")
         self.kalman, self.idle_cfg = kalman, idle_cfg
-        self.n_steps, self.n_streams = packed.slowdown.shape
+        self.n_steps, n_rows = packed.slowdown.shape
+        self.n_streams = n_rows if stream_row is None else len(stream_row)
         self.chunk = min(chunk_steps, self.n_steps)
         d = eng.tdev
-        # pinned host copy of the inputs (outside any timed region)
-        self.host = torch.from_numpy(np.ascontiguousarray(packed.slowdown)).pin_memory()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        # pinned host copies of the inputs (outside any timed region)
+        self.host = pin(packed.slowdown)
         self.seg = [torch.from_numpy(a).to(d) for a in (packed.n_segments, packed.seg_end, packed.seg_phase,
                                                         packed.seg_idle)]
-        self.ss = None if stream_spec is None else torch.as_tensor(np.asarray(stream_spec, np.int32)).to(d)
-        self.bufs = [torch.empty((self.chunk, self.n_streams), dtype=self.host.dtype, device=d) for _ in range(2)]
+        self.goals = None
+        if getattr(packed, "goal_n", None) is not None:
+            self.goals = [torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(d)
+                          for a in (packed.goal_n, packed.goal_end, packed.goal_spec)]
+        ss = (np.arange(self.n_streams) % len(self.specs)).astype(np.int32) if stream_spec is None \
+            else np.asarray(stream_spec, np.int32)
+        # launches: contiguous runs of one goal mode (rows with goal changes: one launch)
+        if self.goals is None:
+            runs = mode_runs(self.specs, ss)
+        else:
+            runs = [(0, self.n_streams, self.specs, ss)]
+        self.runs = [(b, e, sp) for b, e, sp, _ in runs]
+        self.map_host = [pin(np.stack([full for _, _, _, full in runs]))]
+        self.map_dev = [torch.empty_like(self.map_host[0], device=d)]
+        if stream_row is not None:
+            self.map_host.append(pin(np.asarray(stream_row, np.int32)))
+            self.map_dev.append(torch.empty_like(self.map_host[1], device=d))
+        self.bufs = [torch.empty((self.chunk, n_rows), dtype=self.host.dtype, device=d) for _ in range(2)]
         self.copy_stream = torch.cuda.Stream(d)
         self.agg_host = torch.empty((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64).pin_memory()
 
     @property
     def h2d_bytes(self) -> int:
-        return self.host.numel() * self.host.element_size()
+        return self.host.numel() * self.host.element_size() + sum(m.numel() * m.element_size()
+                                                                   for m in self.map_host)
 
     @property
     def d2h_bytes(self) -> int:
@@ -220,9 +241,12 @@ class HostStreamer:
         torch, eng = self.torch, self.eng
         comp = torch.cuda.current_stream(eng.tdev)
         self.copy_stream.wait_stream(comp)  # copies are ordered after the caller's prior work
+        for h, dv in zip(self.map_host, self.map_dev):
+            dv.copy_(h, non_blocking=True)
         state = eng.new_state(self.table, self.n_streams, self.kalman, self.idle_cfg)
         agg = torch.zeros((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64, device=eng.tdev)
         out = outputs_struct(None, agg=agg)
+        stream_row = self.map_dev[1] if len(self.map_dev) > 1 else None
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         consumed = [torch.cuda.Event(), torch.cuda.Event()]
         starts = list(range(0, self.n_steps, self.chunk))
@@ -244,10 +268,13 @@ class HostStreamer:
                 issue_copy(i + 1)
             b = i % 2
             comp.wait_event(copied[b])
-            tr = DeviceTrace(self.bufs[b][: s1 - s0], *self.seg, stream_row=None, step_offset=s0)
-            eng.run(self.table, self.specs, tr, state, policy=self.policy, kalman=self.kalman,
-                    idle_cfg=self.idle_cfg, stream_spec=self.ss, outputs=out, stream_end=self.n_streams,
-                    step_begin=s0, step_end=s1)
+            tr = DeviceTrace(self.bufs[b][: s1 - s0], *self.seg, stream_row=stream_row, step_offset=s0)
+            if self.goals is not None:
+                tr.goal_n, tr.goal_end, tr.goal_spec = self.goals
+            for k, (lb, le, sp) in enumerate(self.runs):
+                eng.run(self.table, sp, tr, state, policy=self.policy, kalman=self.kalman,
+                        idle_cfg=self.idle_cfg, stream_spec=self.map_dev[0][k], outputs=out, stream_begin=lb,
+                        stream_end=le, step_begin=s0, step_end=s1)
             consumed[b].record(comp)
         self.agg_host.copy_(agg, non_blocking=True)
         return self.agg_host

@@ -4,7 +4,8 @@ Restates the reference generator (pkg/src/alertsim/synth.py:21-175) value for
 value — the benchmark configurations of BASELINE.json are defined on its
 tables (the 8x5 preset, 55 candidates; the 64x32 sweep table, 2,144
 candidates) — so the GPU box can build them without the reference installed.
-tests/test_golden.py checks the tables against the reference's own output.
+tests/test_host.py (test_generate_space_equals_reference) checks the tables against the
+reference's own output.
 """
 
 from __future__ import annotations

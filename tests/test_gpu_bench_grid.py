@@ -1,0 +1,191 @@
+"""The benchmark's own workloads through the CUDA engine, checked against the
+CPU oracle (VERDICT r1 "next" #1):
+
+* c4 / c5: scenarios of bench.py's real goal grid (8,192 goal tuples: both
+  modes, deadlines 0.4-2.0 x ref, q_goal 0.30-0.97 / e_goal 0.2-1.0 x P_max x t,
+  max-accuracy without pr_threshold) over its shared 1,000-step permuted-phase
+  traces on the 64x32 table (2,144 candidates), with the grid's extremes
+  forced in; ``alert`` teacher-forced and ``alert+oracle`` (the oracle's own
+  decision stream) against oracle.run.
+* multi-rank: two processes (gloo, both on cuda:0) each run alert_run on
+  their dist.shard range; the per-stream blocks equal the single-process
+  run's bit for bit and the reduced total equals the rank-ordered sum of the
+  per-shard reductions (dist.reduce_aggregates).
+"""
+
+import importlib.util
+import os
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+import paper_1911_00119_b200 as A  # noqa: E402
+from paper_1911_00119_b200 import abi  # noqa: E402
+from paper_1911_00119_b200.trace import unpack_row  # noqa: E402
+from oracle import oracle  # noqa: E402
+
+ROOT = Path(__file__).resolve().parents[1]
+EXEMPT_GAP = 1e-12
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", ROOT / "bench.py")
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    oracle.build()
+
+
+@pytest.fixture(scope="module")
+def grid():
+    b = _bench()
+    total = 16 * 2048
+    wl = b.build_workload("c4", 1000, 0, total, total)  # 16 goal tuples spread over the grid x all traces
+    rng = np.random.default_rng(2026)
+    pick = list(rng.choice(total, 48, replace=False))
+    ss = list(wl["stream_spec"][pick])
+    sr = list(wl["stream_row"][pick])
+    # extremes of the grid: both modes x deadline 0.4 / 2.0 x goal q 0.30 / 0.97 (e_goal 0.2 / 1.0 x P t)
+    for mode in (0, 1):
+        for dm in (0, 63):
+            for g in (0, 63):
+                for trace in (int(rng.integers(2048)), int(rng.integers(2048))):
+                    ss.append(mode * 4096 + dm * 64 + g)
+                    sr.append(trace)
+    ss, sr = np.asarray(ss, np.int32), np.asarray(sr, np.int32)
+    order = np.argsort(wl["specs"]["mode"][ss], kind="stable")  # as the bench: one run per mode
+    return b, wl, ss[order], sr[order]
+
+
+def _oracle_runs(wl, ss, sr, policy):
+    def one(k):
+        env = unpack_row(wl["packed"], int(sr[k]))
+        idx = np.full(len(env.slowdown), int(ss[k]), np.int32)
+        return oracle.run_goals(wl["space"], wl["specs"], idx, env, policy)
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:  # ctypes releases the GIL
+        return list(ex.map(one, range(len(ss))))
+
+
+@pytest.mark.parametrize("policy", ["alert", "alert+oracle"])
+def test_bench_grid_scenarios_vs_oracle(grid, policy):
+    b, wl, ss, sr = grid
+    assert set(wl["specs"]["mode"][ss].tolist()) == {0, 1}
+    assert not wl["specs"]["has_pr"][ss].any()  # the grid's max-accuracy half has no pr_threshold
+    recs = _oracle_runs(wl, ss, sr, policy)
+    forced = np.stack([r[0]["cand"] for r in recs], 1).astype(np.int32)
+    res = A.run_batch(wl["space"], wl["specs"], wl["packed"], policy, stream_spec=ss, stream_row=sr,
+                      records="f64", forced=forced)
+    d = res.decoded()
+    n_ex = 0
+    for k, (rec, agg, st) in enumerate(recs):
+        bad = np.flatnonzero(d["cand"][:, k] != rec["cand"])
+        for n in bad:
+            assert rec["gap"][n] <= EXEMPT_GAP or rec["boundary"][n] <= EXEMPT_GAP, (
+                f"scenario {k} (spec {ss[k]}, trace {sr[k]}) step {n}: GPU {d['cand'][n, k]} vs {rec['cand'][n]}")
+        n_ex += len(bad)
+        np.testing.assert_array_equal(d["met"][:, k], rec["met"])
+        for f in ("energy", "accuracy", "latency", "mu", "sigma2"):
+            np.testing.assert_allclose(res.records[f][:, k], rec[f], rtol=1e-12, err_msg=f"{k}:{f}")
+        np.testing.assert_allclose(res.agg[k, :abi.AGG_LEVEL0], agg[:abi.AGG_LEVEL0], rtol=1e-12)
+        if policy == "alert+oracle":
+            np.testing.assert_array_equal(res.oracle_decision[:, k] & 0xFFFF, rec["or_cand"], err_msg=str(k))
+            np.testing.assert_allclose(res.agg[k, abi.AGG_OR_ENERGY:abi.AGG_OR_SAME + 1],
+                                       agg[abi.AGG_OR_ENERGY:abi.AGG_OR_SAME + 1], rtol=1e-12)
+    assert n_ex <= 1e-3 * forced.size
+    # the grid really exercises the fallback levels and the FP64 re-rank the bench reports
+    levels = d["level"]
+    assert (levels > 0).any() and (levels == 0).any()
+
+
+def test_bench_grid_free_running_aggregates(grid):
+    """Free-running (no forcing) at the bench's launch configuration: every
+    scenario follows the oracle's trajectory until, at most, a documented
+    ulp-level near-tie; scenarios that never diverge equal the oracle's
+    aggregates and final state (to 1e-12)."""
+    b, wl, ss, sr = grid
+    recs = _oracle_runs(wl, ss, sr, "alert")
+    res = A.run_batch(wl["space"], wl["specs"], wl["packed"], "alert", stream_spec=ss, stream_row=sr,
+                      records="f64")
+    d = res.decoded()
+    same = 0
+    for k, (rec, agg, st) in enumerate(recs):
+        bad = np.flatnonzero(d["cand"][:, k] != rec["cand"])
+        if len(bad):
+            n = bad[0]
+            assert rec["gap"][n] <= EXEMPT_GAP or rec["boundary"][n] <= EXEMPT_GAP, (k, n)
+            continue
+        np.testing.assert_allclose(res.agg[k, :abi.AGG_LEVEL0], agg[:abi.AGG_LEVEL0], rtol=1e-12, err_msg=str(k))
+        np.testing.assert_allclose(res.state["mu"][k], st[0], rtol=1e-12)
+        same += 1
+    assert same >= 0.9 * len(ss)
+
+
+# --- two ranks through alert_run ----------------------------------------------
+
+def _rank_main(rank, world, port, n, out_dir):
+    import sys
+
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1911_00119_b200 as A
+    from paper_1911_00119_b200.dist import reduce_aggregates, shard
+
+    b = _bench()
+    s, e = shard(n, world, rank)
+    wl = b.build_workload("c2", 600, s, e, n)
+    eng = A.get_engine(0)
+    res = A.run_batch(wl["space"], wl["specs"], wl["packed"], "alert", stream_spec=wl["stream_spec"],
+                      trace_dtype=np.float32, keep_on_device=True)
+    local = eng.reduce(res.agg).cpu()
+    total = reduce_aggregates(local)  # gloo all_gather, summed in rank order
+    np.save(os.path.join(out_dir, f"agg{rank}.npy"), res.agg.cpu().numpy())
+    np.save(os.path.join(out_dir, f"local{rank}.npy"), local.numpy())
+    np.save(os.path.join(out_dir, f"total{rank}.npy"), total.numpy())
+    dist.destroy_process_group()
+
+
+def test_two_ranks_through_alert_run_equal_one(tmp_path):
+    import socket
+
+    import torch.multiprocessing as mp
+
+    n, world = 3000, 2
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    mp.start_processes(_rank_main, args=(world, port, n, str(tmp_path)), nprocs=world, start_method="spawn")
+    b = _bench()
+    wl = b.build_workload("c2", 600, 0, n, n)
+    eng = A.get_engine(0)
+    one = A.run_batch(wl["space"], wl["specs"], wl["packed"], "alert", stream_spec=wl["stream_spec"],
+                      trace_dtype=np.float32, keep_on_device=True)
+    parts = [np.load(tmp_path / f"agg{r}.npy") for r in range(world)]
+    np.testing.assert_array_equal(np.concatenate(parts), one.agg.cpu().numpy())  # per stream: bit for bit
+    t0, t1 = np.load(tmp_path / "total0.npy"), np.load(tmp_path / "total1.npy")
+    np.testing.assert_array_equal(t0, t1)  # every rank holds the same total
+    from paper_1911_00119_b200.dist import shard
+
+    expect = sum(eng.reduce(one.agg[slice(*shard(n, world, r))]).cpu().numpy() for r in range(world))
+    np.testing.assert_array_equal(t0, expect)  # = rank-ordered sum of the per-shard reductions
+    whole = eng.reduce(one.agg).cpu().numpy()
+    np.testing.assert_allclose(t0, whole, rtol=1e-14)
+    assert t0[abi.AGG_N] == n * 600
