@@ -386,7 +386,7 @@ def python_reference(wl, policy: str, seconds: float = 8.0):
         t0 = time.perf_counter()
         done = sum(pool.map(_py_ref_stream, jobs(ns, steps), chunksize=1))
         dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "decisions/s", "cores": ns, "kind": "reference-python",
+    return {"value": done / dt, "unit": "decisions/s", "cores": min(cores, ns), "kind": "reference-python",
             "cpu_model": cpu_model(),
             "sample": f"{ns} items x {steps} steps of {wl['desc']} ({policy}): alertsim.simulator.run + make_policy "
                       f"(baseline/_ref, Python {sys.version.split()[0]}), multiprocessing.Pool({cores}), {dt:.1f} s"}

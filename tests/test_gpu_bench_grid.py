@@ -187,5 +187,5 @@ def test_two_ranks_through_alert_run_equal_one(tmp_path):
     expect = sum(eng.reduce(one.agg[slice(*shard(n, world, r))]).cpu().numpy() for r in range(world))
     np.testing.assert_array_equal(t0, expect)  # = rank-ordered sum of the per-shard reductions
     whole = eng.reduce(one.agg).cpu().numpy()
-    np.testing.assert_allclose(t0, whole, rtol=1e-14)
+    np.testing.assert_allclose(t0, whole, rtol=1e-12)  # another summation grouping
     assert t0[abi.AGG_N] == n * 600
