@@ -504,16 +504,15 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if trace_bytes < 126e6 else None
 
     def step(timed: bool):
-        state = eng.new_state(table, S)
-        agg.zero_()
+        state = eng.new_state(table, S, init=False)  # initialised by the launch (FLAG_FRESH)
         if flush is not None:
             flush.fill_(1)
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
         for lb, le, lsp, lss in launches:
-            eng.run(table, lsp, trace, state, policy=pol, stream_spec=lss, outputs=out, flags=args.flags,
-                    stream_begin=lb, stream_end=le)
+            eng.run(table, lsp, trace, state, policy=pol, stream_spec=lss, outputs=out,
+                    flags=args.flags | abi.FLAG_FRESH, stream_begin=lb, stream_end=le)
         if timed:
             b.record(stream)
             kev.append((a, b))

@@ -37,9 +37,10 @@
 extern "C" {
 #endif
 
-#define ALERT_ABI_VERSION 3  /* 2: comparison-scheme policies, AlertSpaceDesc.sys_dnn/app_dnn, AlertState.policy_aux, AlertOutputs.fb_*, alert_xi_stats
+#define ALERT_ABI_VERSION 4  /* 2: comparison-scheme policies, AlertSpaceDesc.sys_dnn/app_dnn, AlertState.policy_aux, AlertOutputs.fb_*, alert_xi_stats
                                3: goal schedules (AlertTrace.goal_*), AlertOutputs.plan_goal/phi, decision bit 30
-                                  (feasible), alert_baseline_decide / alert_static_choice (per-step comparison schemes) */
+                                  (feasible), alert_baseline_decide / alert_static_choice (per-step comparison schemes)
+                               4: ALERT_FLAG_FRESH (state initialised / aggregates zeroed inside alert_run) */
 
 /* ---- status codes ------------------------------------------------------ */
 typedef enum AlertStatus {
@@ -79,6 +80,10 @@ enum { ALERT_DTYPE_F32 = 0, ALERT_DTYPE_F64 = 1 };
 #define ALERT_FLAG_NO_FAST 0x4u    /* disable the min-energy fast scan (full FP32 scan every step; A/B and tests) */
 #define ALERT_FLAG_FAST_ROWS 0x8u  /* fast scan in row mode even for small tables (tests) */
 #define ALERT_FLAG_ANY_WINDOW 0x10u /* anytime cells by the two-pass window instead of column skips (A/B, tests) */
+#define ALERT_FLAG_NO_ORACLE_FAST 0x40u /* oracle: full scan only (no certified min-energy fast scan; A/B, tests) */
+#define ALERT_FLAG_FRESH 0x20u     /* the step range starts the runs: the filter state is initialised in the
+                                    * launch (state arrays written, not read: no alert_state_init needed) and
+                                    * the aggregate blocks are written from zero (not accumulated: no memset) */
 
 /* Compiled limits */
 #define ALERT_MAX_STAGES 8         /* stages per anytime DNN                   */

@@ -5,11 +5,13 @@ missing, every entry point raises."""
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from . import abi
 
-LIB_PATH = Path(__file__).resolve().parent / "libalert_b200.so"
+# ALERT_LIB_PATH: an experimental build variant of the same sources (A/B runs)
+LIB_PATH = Path(os.environ.get("ALERT_LIB_PATH") or Path(__file__).resolve().parent / "libalert_b200.so")
 
 EXPORTS = (
     "alert_abi_version", "alert_strerror", "alert_last_error", "alert_create", "alert_destroy",

@@ -6,7 +6,7 @@ import ctypes as C
 
 import numpy as np
 
-ALERT_ABI_VERSION = 3
+ALERT_ABI_VERSION = 4
 
 KIND_TRADITIONAL, KIND_ANYTIME = 0, 1
 MODE_MIN_ENERGY, MODE_MAX_ACCURACY = 0, 1
@@ -20,6 +20,8 @@ FLAG_NO_REFINE = 0x2
 FLAG_NO_FAST = 0x4  # disable the min-energy fast scan (A/B, tests)
 FLAG_FAST_ROWS = 0x8  # fast scan in row mode (default for > 512 traditional cells)
 FLAG_ANY_WINDOW = 0x10  # anytime cells by the two-pass window (A/B, tests)
+FLAG_NO_ORACLE_FAST = 0x40  # oracle full scan only (A/B)
+FLAG_FRESH = 0x20  # step range starts the runs: state initialised and aggregates zeroed in the launch
 MAX_STAGES = 8
 MAX_PHASES = 8
 MAX_CANDIDATES = 6144

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -526,39 +527,62 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     unit_lb[k] = (float)(2.0 - units[k].bound) - 1e-5f;
   }
   // the same order flattened to one entry per cell for the W = 1 scan
-  // (fast_max_accuracy_flat, tables of <= 64 cells): the cell's cellA row and
-  // {cell | k << 7 | anytime << 10 | next group << 11 | next unit << 18, unit
-  // lb bits}, k = stage within the unit.  A group = the run of units of one
-  // DNN (equal bounds), re-ordered by latency ascending: a unit whose
-  // deadline-probability bound fails makes every later unit of the group fail
-  // too (1/t only falls), so the scan skips the group.
-  std::vector<float4> seqA;
-  std::vector<int2> seqM;
+  // (fast_max_accuracy_flat, tables of <= 64 cells), one sequence per DNN-kinds
+  // filter (1 traditional, 2 anytime, 3 both; the excluded units are left
+  // out): the cell's cellA row (.w = q_fail at a unit start, 0 after: the
+  // running accuracy restarts by acc * carry + .w) and the metadata {unit lb,
+  // dead-group multiplier (1 at a unit start whose group the deadline bound
+  // can kill, else 0), carry (0 at a unit start, else 1), k | cell << 8 |
+  // (skip to - 1) << 16 | (chain out to - 1) << 24}.  A group = the run of
+  // units of one DNN (equal bounds), re-ordered by latency ascending: a unit
+  // whose deadline-probability bound fails makes every later unit of the
+  // group fail too (1/t only falls), so the scan skips the group; an anytime
+  // unit's first cell can kill its group only with monotone stage latencies
+  // (any_mono), which is also when a surely infeasible stage ends its chain.
+  bool mono = true;
+  for (const int2& cd : cols)
+    for (int k = 1; k < cd.y; ++k)
+      if (!(c64[cd.x + k].t >= c64[cd.x + k - 1].t)) mono = false;
+  std::vector<float4> seqA[3], seqM[3];
   if (n <= 64) {
-    for (size_t g0 = 0; g0 < units.size();) {
-      const int dnn = tb->cand_dnn[order[units[g0].first]];
-      size_t g1 = g0 + 1;
-      while (g1 < units.size() && tb->cand_dnn[order[units[g1].first]] == dnn) ++g1;
-      std::vector<Unit> grp(units.begin() + g0, units.begin() + g1);
-      std::stable_sort(grp.begin(), grp.end(),
-                       [&](const Unit& a, const Unit& b) { return c64[a.first].t < c64[b.first].t; });
-      int cells = 0;
-      for (const Unit& u : grp) cells += u.n & 0xFFFF;
-      const int next_group = (int)seqM.size() + cells;
-      for (const Unit& u : grp) {
-        const int m = u.n & 0xFFFF, next = (int)seqM.size() + m;
-        const float lb = (float)(2.0 - u.bound) - 1e-5f;
-        int lbi;
-        memcpy(&lbi, &lb, 4);
-        for (int k = 0; k < m; ++k) {
-          seqA.push_back(A[u.first + k]);
-          seqM.push_back(make_int2((u.first + k) | (k << 7) | ((u.n >> 16) << 10) | (next_group << 11) | (next << 18),
-                                   lbi));
+    for (int kinds = 1; kinds <= 3; ++kinds) {
+      std::vector<Unit> ku;
+      for (const Unit& u : units)
+        if ((kinds >> ((u.n >> 16) ? 1 : 0)) & 1) ku.push_back(u);
+      auto& SA = seqA[kinds - 1];
+      auto& SM = seqM[kinds - 1];
+      for (size_t g0 = 0; g0 < ku.size();) {
+        const int dnn = tb->cand_dnn[order[ku[g0].first]];
+        size_t g1 = g0 + 1;
+        while (g1 < ku.size() && tb->cand_dnn[order[ku[g1].first]] == dnn) ++g1;
+        std::vector<Unit> grp(ku.begin() + g0, ku.begin() + g1);
+        std::stable_sort(grp.begin(), grp.end(),
+                         [&](const Unit& a, const Unit& b) { return c64[a.first].t < c64[b.first].t; });
+        int cells = 0;
+        for (const Unit& u : grp) cells += u.n & 0xFFFF;
+        const int next_group = (int)SM.size() + cells;
+        for (const Unit& u : grp) {
+          const int m = u.n & 0xFFFF, next = (int)SM.size() + m;
+          const bool any = (u.n >> 16) != 0;
+          const float lb = (float)(2.0 - u.bound) - 1e-5f;
+          for (int k = 0; k < m; ++k) {
+            const int here = (int)SM.size();
+            float4 a = A[u.first + k];
+            a.w = k == 0 ? a.w : 0.0f;
+            SA.push_back(a);
+            const int out_to = (any && mono) ? next : here + 1;
+            const uint32_t w = (uint32_t)k | ((uint32_t)(u.first + k) << 8) | ((uint32_t)(next_group - 1) << 16) |
+                               ((uint32_t)(out_to - 1) << 24);
+            float wf;
+            memcpy(&wf, &w, 4);
+            SM.push_back(make_float4(lb, (k == 0 && (!any || mono)) ? 1.0f : 0.0f, k == 0 ? 0.0f : 1.0f, wf));
+          }
         }
+        g0 = g1;
       }
-      g0 = g1;
     }
   }
+  const size_t n_seq = std::max(seqM[0].size(), std::max(seqM[1].size(), seqM[2].size()));
   // min-energy row mode: traditional DNN rows {dnn bits, smallest cap * t,
   // largest 1/t, 0} by their smallest cap * t, ascending
   std::vector<float4> trows;
@@ -577,7 +601,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   }
   size_t oTrows = place(sizeof(float4) * trows.size());
   size_t oUnit = place(sizeof(int2) * units.size()), oUlb = place(4 * units.size());
-  size_t oSeqA = place(sizeof(float4) * seqA.size()), oSeqM = place(sizeof(int2) * seqM.size());
+  size_t oSeqA = place(sizeof(float4) * 3 * n_seq), oSeqM = place(sizeof(float4) * 3 * n_seq);
   // comparison-scheme cells (policies.py:283-454): per power, the sys-only
   // DNN's cell and the first cell of the app-only DNN's column
   std::vector<int> sys_cells(P, -1), app_first(P, -1);
@@ -610,10 +634,11 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     memcpy(&h[oUlb], unit_lb.data(), 4 * units.size());
   }
   if (!trows.empty()) memcpy(&h[oTrows], trows.data(), sizeof(float4) * trows.size());
-  if (!seqM.empty()) {
-    memcpy(&h[oSeqA], seqA.data(), sizeof(float4) * seqA.size());
-    memcpy(&h[oSeqM], seqM.data(), sizeof(int2) * seqM.size());
-  }
+  for (int v = 0; v < 3; ++v)
+    if (!seqM[v].empty()) {
+      memcpy(&h[oSeqA + sizeof(float4) * v * n_seq], seqA[v].data(), sizeof(float4) * seqA[v].size());
+      memcpy(&h[oSeqM + sizeof(float4) * v * n_seq], seqM[v].data(), sizeof(float4) * seqM[v].size());
+    }
   memcpy(&h[oApp], app_first.data(), 4 * P);
   e = cudaMemcpy(buf, h.data(), bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -638,19 +663,18 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   T.units = units.empty() ? nullptr : reinterpret_cast<const int2*>(buf + oUnit);
   T.unit_lb = units.empty() ? nullptr : reinterpret_cast<const float*>(buf + oUlb);
   T.n_units = (int)units.size();
-  T.useqA = seqM.empty() ? nullptr : reinterpret_cast<const float4*>(buf + oSeqA);
-  T.useqM = seqM.empty() ? nullptr : reinterpret_cast<const int2*>(buf + oSeqM);
-  T.n_seq = (int)seqM.size();
+  T.useqA = n_seq ? reinterpret_cast<const float4*>(buf + oSeqA) : nullptr;
+  T.useqM = n_seq ? reinterpret_cast<const float4*>(buf + oSeqM) : nullptr;
+  T.n_seq = (int)n_seq;
+  T.n_seqk[0] = 0;
+  for (int v = 0; v < 3; ++v) T.n_seqk[v + 1] = (int)seqM[v].size();
   T.trad_rows = trows.empty() ? nullptr : reinterpret_cast<const float4*>(buf + oTrows);
   T.app_first = app_stages > 0 ? reinterpret_cast<const int*>(buf + oApp) : nullptr;
   T.app_stages = app_stages;
   T.cap_max = (float)max_cap;
   T.cap_min = (float)d->power_cap[0];
   for (int j = 1; j < P; ++j) T.cap_min = std::min(T.cap_min, (float)d->power_cap[j]);
-  T.any_mono = 1;  // fast scan's anytime skip (fast_min_energy): stage latencies non-decreasing
-  for (const int2& cd : cols)
-    for (int k = 1; k < cd.y; ++k)
-      if (!(c64[cd.x + k].t >= c64[cd.x + k - 1].t)) T.any_mono = 0;
+  T.any_mono = mono;  // fast scans' anytime skips: stage latencies non-decreasing
   tb->buf = buf;
   tb->n_cand = n;
   tb->n_any_cols = (int)cols.size();
@@ -715,6 +739,7 @@ static size_t table_smem(const AlertTable* tb, int W) {
 static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_specs, int tpb, int W, RunParams& P,
                         int policy = ALERT_POLICY_ALERT, unsigned flags = 0) {
   const DevTable& T = tb->dev;
+  P.policy = policy;
   // min-energy fast scan (fast_min_energy): needs some min-energy spec, row /
   // column indices that fit the 6-bit key field, and the ALERT policy family
   bool any_min_energy = false, all_min_energy = true;
@@ -723,6 +748,10 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
     all_min_energy &= specs[k].mode == ALERT_MODE_MIN_ENERGY;
   }
   P.min_energy_only = all_min_energy;
+  P.any_min_energy = any_min_energy;
+  // few specs: staged once per block (a tile's spec is a pointer), else one copy per tile
+  static const bool no_shared_specs = std::getenv("ALERT_NO_SPEC_SHARED") != nullptr;  // A/B knob
+  P.spec_shared = !no_shared_specs && n_specs <= kSpecSmemMax && n_specs < tpb / W;
   const int n_tdnn = T.n_powers > 0 ? T.n_trad / T.n_powers : 0;
   P.zlo = nullptr;
   P.fast_smem = 0;
@@ -733,7 +762,7 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
   if ((any_min_energy || any_max_accuracy) && policy != ALERT_POLICY_ORACLE &&
       !(flags & (ALERT_FLAG_NO_FAST | ALERT_FLAG_FP64_ALL)) &&
       ALERT_MAX_STAGES <= 8 &&
-      (P.fast_rows || (size_t)(tpb / W) * (size_t)(n_tdnn + 1) * 2 * sizeof(float) <= 16 * 1024))
+      (P.fast_rows || !any_min_energy || (size_t)(tpb / W) * (size_t)T.n_trad * sizeof(float) <= 16 * 1024))
     P.fast_smem = 1;  // alert_run computes the thresholds (zlo_kernel) and sets P.zlo
   // max-accuracy fast scan needs its sorted units in shared memory
   if (P.fast_smem && any_max_accuracy && T.units && T.n_units <= 1024) P.units_smem = 1;
@@ -745,14 +774,18 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
   bool refine_heavy = false;
   for (int k = 0; k < n_specs; ++k)
     refine_heavy |= specs[k].mode == ALERT_MODE_MAX_ACCURACY && specs[k].has_pr;
-  P.sv_smem = refine_heavy && (size_t)(tpb / W) * (size_t)T.n_cells * sizeof(float) <= 32 * 1024;
+  // (not with the one-lane flat max-accuracy scan: it keeps no per-cell
+  // objectives, and the slots would only cost occupancy)
+  const bool flat = W == 1 && T.n_seq > 0 && P.units_smem;
+  P.sv_smem = refine_heavy && !flat && (size_t)(tpb / W) * (size_t)T.n_cells * sizeof(float) <= 32 * 1024;
 }
 
 static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const RunParams& P) {
   const DevTable& T = tb->dev;
-  SmemLayout L(T.n_cells, T.n_any_cols, tpb / W, P.c64_smem ? T.n_cells : 0, tpb / W,
-               P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
-               (P.fast_smem && !P.fast_rows) ? T.n_trad / T.n_powers : 0,
+  const size_t agg_bytes = P.policy == ALERT_POLICY_ALERT_WITH_ORACLE ? sizeof(TileAggOr) : sizeof(TileAgg);
+  SmemLayout L(T.n_cells, T.n_any_cols, P.spec_shared ? n_specs : tpb / W, P.c64_smem ? T.n_cells : 0, tpb / W,
+               P.ratio_smem ? T.n_powers : 0, agg_bytes, P.sv_smem ? T.n_cells : 0, W,
+               (P.fast_smem && !P.fast_rows && P.any_min_energy) ? T.n_trad : 0,
                (P.fast_smem && !P.fast_rows) ? T.n_trad : 0, P.fast_smem && !P.fast_rows,
                P.units_smem ? T.n_units : 0, P.units_smem ? T.n_seq : 0);
   return L.total;
@@ -944,6 +977,21 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
       (out->stream_stride == 0 && out->step_stride == 0))
     return fail(ALERT_ERR_INVALID_ARGUMENT, "alert_run: per-step outputs need strides");
   if (stream_end == stream_begin || step_end == step_begin) return ALERT_OK;
+  if (baseline && (flags & ALERT_FLAG_FRESH)) {  // the fused comparison schemes read state / accumulate
+    CUDA_TRY(cudaSetDevice(ctx->device));
+    const long long nr = stream_end - stream_begin;
+    AlertState sub = st;
+    sub.mu += stream_begin; sub.sigma2 += stream_begin; sub.k_gain += stream_begin; sub.q_noise += stream_begin;
+    sub.innov += stream_begin; sub.phi += stream_begin; sub.m_var += stream_begin;
+    sub.group_budget += stream_begin; sub.group_count += stream_begin;
+    if (sub.policy_aux) sub.policy_aux += stream_begin;
+    state_init_kernel<<<(unsigned)((nr + 255) / 256), 256, 0, (cudaStream_t)cuda_stream>>>(sub, *cfg, tb->dev.phi0, nr);
+    CUDA_TRY(cudaGetLastError());
+    ctx->launches++;
+    if (out->agg)
+      CUDA_TRY(cudaMemsetAsync(out->agg + stream_begin * ALERT_AGG_FIELDS, 0, sizeof(double) * ALERT_AGG_FIELDS * nr,
+                               (cudaStream_t)cuda_stream));
+  }
   if (baseline) return run_baseline(ctx, tb, cfg, specs, n_specs, stream_spec, tr, st, out, policy, stream_begin,
                                     stream_end, step_begin, step_end, (cudaStream_t)cuda_stream);
   int W = pick_lanes(ctx, tb);
@@ -1002,7 +1050,10 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
     ctx->launches++;
     P.zlo = dzlo;
   }
+  P.work = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&P.work, sizeof(unsigned long long), s));  // persistent work counter
   r = dispatch_run(W, pf, P, tpb, smem, s);
+  cudaFreeAsync(P.work, s);
   cudaFreeAsync(dspecs, s);
   if (dzlo) cudaFreeAsync(dzlo, s);
   if (r) return r;

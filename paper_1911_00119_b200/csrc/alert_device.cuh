@@ -56,11 +56,15 @@ struct DevTable {
   const int2* units;      // {first cell, n cells | anytime << 16}
   const float* unit_lb;   // lower bound of any key of the unit: 2 - bound - 1e-5
   int n_units;
-  // units flattened per cell (tables of <= 64 cells, else n_seq = 0): cellA
-  // rows and {cell | k << 7 | anytime << 10 | next group << 11 | next unit << 18, lb}
+  // units flattened per cell (tables of <= 64 cells, else n_seq = 0), one
+  // sequence per DNN-kinds filter (kinds 1, 2, 3 at offsets 0, n_seq, 2 n_seq):
+  // cellA rows (.w = q_fail at a unit start, 0 after) and {unit lb, dead-group
+  // multiplier, chain carry, k | cell << 8 | (skip to) - 1 << 16 | (chain out
+  // to) - 1 << 24} (fast_max_accuracy_flat)
   const float4* useqA;
-  const int2* useqM;
-  int n_seq;
+  const float4* useqM;
+  int n_seq;       // the longest sequence (shared-memory slots)
+  int n_seqk[4];   // length per kinds (index 1..3)
   const float4* trad_rows;  // min-energy row mode: {dnn bits, min cap * t, max 1/t, 0}, min cap * t ascending
   float cap_min;            // smallest cap (FP32)
 
@@ -188,8 +192,9 @@ struct StepCtx {
   bool any_window;      // ALERT_FLAG_ANY_WINDOW: two-pass window for anytime cells (A/B)
   const int2* su;       // max-accuracy fast scan: units / key lower bounds staged in shared memory
   const float* slb;
-  const float4* sqA;    // T.useqA / T.useqM staged in shared memory (or null)
-  const int2* sqM;
+  const float4* sqA;    // the kinds' T.useqA / T.useqM sequence staged in shared memory (or null)
+  const float4* sqM;
+  int n_seq;            // its length
   float hs, hm;      // T_d = fma(z'_d, hs, hm)
   float Tpr;     // same for the pr_threshold z-bound (anytime cells)
 };
@@ -218,6 +223,7 @@ __device__ __forceinline__ void make_ctx(StepCtx& x, const SpecDev* sp, const Ce
   x.slb = nullptr;
   x.sqA = nullptr;
   x.sqM = nullptr;
+  x.n_seq = 0;
   x.any_window = false;
   x.hs = x.hm = 0.f;
   x.Tpr = -kInfF;
@@ -709,10 +715,11 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
       }
     }
   } else if (kinds & 1) {
-    const char* tb = reinterpret_cast<const char*>(x.tT);
+    const float* zt = x.tT;  // the tile's z' per traditional cell, element c at zt[c * tS]
+    const int tS = x.tS;
     const float4* sF = x.sF;
-    auto key_of = [&](const float4& F) {  // F.w = the cell's position in its chunk
-      const float Td = fmaf(*reinterpret_cast<const float*>(tb + __float_as_int(F.z)), x.hs, x.hm);
+    auto key_of = [&](const float4& F, int c) {  // F.w = the cell's position in its chunk
+      const float Td = fmaf(zt[c * tS], x.hs, x.hm);
       return pack_key(F.y * fmax3(x.mu_e, fmaf(x.phig, F.x, x.ompmu), fmaf(mgH, F.x, Td)), __float_as_uint(F.w));
     };
     const int n = T.n_trad;
@@ -721,7 +728,7 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
       const float s1 = t.p1;
       float k[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) k[u] = key_of(sF[c + u * W]);
+      for (int u = 0; u < 8; ++u) k[u] = key_of(sF[c + u * W], c + u * W);
 #pragma unroll
       for (int u = 0; u < 8; u += 2) t.push2(k[u], k[u + 1]);
       if (t.p1 != s1) t.blk = c;
@@ -736,7 +743,8 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
         float k[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float kk = key_of(sF[c + u * W]);  // padded table: reads past the end are masked
+          // padded tables: reads past the end are masked (the z' index clamped)
+          const float kk = key_of(sF[c + u * W], min(c + u * W, n - 1));
           k[u] = c + u * W < n ? kk : kInfF;
         }
         t.push2(k[0], k[1]);
@@ -1124,24 +1132,28 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
 
 // W = 1, up to 64 cells (the preset-sized tables): the same certified scan
 // with the bound-ordered units flattened to one loop over their cells
-// (T.useq), so every lane issues the same cell body each iteration instead of
+// (T.useq, one sequence per DNN-kinds filter, so excluded units are simply
+// absent), so every lane issues the same cell body each iteration instead of
 // a divergent chain loop nested in a unit loop; a unit whose first cell fails
 // the deadline-probability bound skips the rest of its DNN's group (units
-// sorted by latency).  Pass 1 runs on until the next unit's bound exceeds
-// both the running P2 and the running tie cut, and marks (64-bit mask over
-// sequence positions) every key within the running cut: the final cut is
+// sorted by latency).  Pass 1 runs on until the next cell's unit bound
+// exceeds both the running P2 and the running tie cut, and marks (64-bit mask
+// over sequence positions) every key within the running cut: the final cut is
 // never larger, so the near-tie pass (c') re-derives only the marked cells.
+// The per-cell body is laid out for the FMA pipe: the sequence metadata
+// {unit lb, dead-group multiplier, chain carry, k | cell << 8 | skip target
+// << 16 | chain-out target << 24} needs no bit-field decoding on the key
+// path, the running accuracy restarts by an FMA with the carry, and the
+// P1 / P2 sentinels (2.5 > any feasible key 2 - acc) need no clamp.
 template <bool HAS_PR>
 __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const float4* __restrict__ sA,
                                                        const float4* __restrict__ sB, const StepCtx& x,
                                                        int kinds, Decision& d) {
   const float mgH = -x.goal_f * kPenH;
   const float elH = -x.e_lo * kPenH;
-  const int n_seq = T.n_seq;
-  const bool mono = T.any_mono;
-  const bool k_trad = kinds & 1, k_any = kinds & 2;
-  // 32-bit shared addresses (no generic-to-shared conversion per cell); the
-  // row and the metadata of an entry are independent loads
+  const float elim = x.e_lo * (1.0f + x.d_erel);  // chain-out energy test (2 d_erel margin)
+  const int n_seq = x.n_seq;
+  // 32-bit shared addresses (no generic-to-shared conversion per cell)
   const unsigned aqa = (unsigned)__cvta_generic_to_shared(x.sqA);
   const unsigned aqm = (unsigned)__cvta_generic_to_shared(x.sqM);
   const unsigned aA = (unsigned)__cvta_generic_to_shared(sA);
@@ -1150,10 +1162,15 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
     asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
     return v;
   };
-  auto meta_at = [&](int i) {
-    int2 v;
-    asm("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(aqm + 8u * i));
+  auto meta_w = [&](int i) {
+    unsigned v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(aqm + 16u * i + 12u));
     return v;
+  };
+  auto shl = [](unsigned v, unsigned s) {  // PTX shl clamps s >= 32 to 0 bits left
+    unsigned r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(v), "r"(s));
+    return r;
   };
   auto cell_at = [&](int c) { return f4(aA + 16u * c); };
   auto energy = [&](const float4& A) { return A.y * fmaxf(x.mu_e, fmaf(x.phig, A.x, x.ompmu)); };
@@ -1162,46 +1179,46 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
     return fmaxf(fmaf(E, kPenH, elH), pp);
   };
   const float dcut = 2.0f * x.d_acc + 4e-6f;  // tie cut above P1: + truncation of both keys
-  Top2 t{kInfF, kInfF, -1};
-  unsigned long long marks = 0ull;
+  float p1 = 2.5f, p2 = 2.5f, pd = 2.5f + dcut;
+  int bi = -1;
+  unsigned mlo = 0u, mhi = 0u;
   float acc = 0.0f;
   for (int i = 0; i < n_seq; ++i) {
     const float4 A = f4(aqa + 16u * i);
-    const int2 M = meta_at(i);
-    const unsigned long long bit = 1ull << i;
-    const int k = (M.x >> 7) & 7;
+    const float4 M = f4(aqm + 16u * i);
+    // stop once no later unit (nor the rest of this one) can be P1, P2 or tied with P1
+    if (M.x >= p2 && M.x > pd) break;
+    const unsigned w = __float_as_uint(M.w);
     const float pp = HAS_PR ? fmaf(mgH, A.x, x.Tpr) : -kInfF;
-    // unit start: stop once no later unit can be P1, P2 or tied with P1
-    const bool start = k == 0;
-    const float lb = __int_as_float(M.y);
-    if (start && lb >= t.p2 && lb > t.p1 + dcut) break;
-    // the rest is predicated (no divergent paths inside the loop): a skipped
-    // group / chain costs one cell body and moves i
-    const bool any = (M.x >> 10) & 1;
-    const bool kok = any ? k_any : k_trad;
-    const bool gdead = pp > 0.0f && (!any || mono);
-    const bool skip = start && (!kok || gdead);  // group out
-    acc = start ? A.w : acc;
+    const bool skip = pp * M.y > 0.0f;  // unit start of a group the deadline bound kills
+    acc = fmaf(acc, M.z, A.w);          // chain carry (0 at a unit start: restart at q_fail)
     const float ph = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
     const float E = energy(A);
     const float pen = fmaxf(fmaf(E, kPenH, elH), pp);
     acc = fmaf(ph, A.z, acc);
     // surely infeasible at L0 (see fast_max_accuracy): no key; with monotone
-    // stage latencies the rest of the chain is out too
+    // stage latencies the rest of the chain is out too (host: target = next
+    // cell when latencies are not monotone)
     const bool out = skip || pen > 0.0f;
     int nxt = i;
-    if (out && mono && (pp > 0.0f || E > x.e_lo * (1.0f + x.d_erel))) nxt = ((M.x >> 18) & 127) - 1;
-    if (skip) nxt = ((M.x >> 11) & 127) - 1;
+    if (out && (pp > 0.0f || E > elim)) nxt = (int)(w >> 24);
+    if (skip) nxt = (int)((w >> 16) & 0xFFu);
+    const float key = out ? kInfF : pack_key(fmaxf(2.0f - acc, pen), w);
+    if (key < p1) bi = i;
+    p2 = fminf(p2, fmaxf(p1, key));
+    p1 = fminf(p1, key);
+    pd = p1 + dcut;
+    if (key <= pd) {
+      mlo |= shl(1u, (unsigned)i);
+      mhi |= shl(1u, (unsigned)(i - 32));
+    }
     i = nxt;
-    const float key = out ? kInfF : pack_key(fmaxf(2.0f - acc, pen), (unsigned)k);
-    const float before = t.p1;
-    t.push(key);
-    if (t.p1 != before) t.blk = (M.x & 127) - k;
-    if (key <= fminf(t.p1 + dcut, 3.0f)) marks |= bit;
   }
-  if (!(t.p1 < 2.0f) || t.blk < 0) return false;  // P1 must be a possible cell (no penalty)
-  const int c1 = t.blk + (int)(__float_as_uint(t.p1) & 7u);
+  if (!(p1 < 2.0f) || bi < 0) return false;  // P1 must be a possible cell (no penalty)
+  const int c1 = (int)((meta_w(bi) >> 8) & 0xFFu);
   if (c1 >= T.n_cells) return false;
+  unsigned long long marks = ((unsigned long long)mhi << 32) | mlo;
+  Top2 t{p1, p2, bi};
   auto sure = [&](int c) {
     const float4 A = cell_at(c);
     if (!(energy(A) <= x.e_hi)) return false;
@@ -1221,8 +1238,8 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
     while (marks) {
       const int i = __ffsll((long long)marks) - 1;
       marks &= marks - 1;
-      const int2 M = meta_at(i);
-      const int k = (M.x >> 7) & 7, c = M.x & 127;
+      const unsigned mw = meta_w(i);
+      const int k = (int)(mw & 7u), c = (int)((mw >> 8) & 0xFFu);
       float a = 0.f, tail = 0.f, r = 0.f;
       bool bad = false;
       float4 A;
@@ -1884,16 +1901,103 @@ __device__ Decision oracle_decide_t(const DevTable& T, const float4* sA, const f
   return d;
 }
 
+// OraclePolicy.decide, min-energy level 0 (policies.py:160-205) as a
+// certified fast scan.  Level 0 needs the input to complete (s t <= goal) and
+// the delivered accuracy >= q_goal; a traditional cell that completes delivers
+// its DNN's accuracy, so a DNN row whose accuracy class fails q_goal can never
+// be feasible and is skipped as a whole (uniform over the tile).  Per cell of
+// the remaining rows: energy E (as or_cell) and a sign-exact deadline penalty
+// H (s t - goal (1 + 8 eps)) > 0 for cells that surely miss; the key is their
+// max, so possible cells (surely or maybe completing) compete on energy.
+// Anytime columns run the column logic of or_cell (possible = sure or
+// uncertain at level 0).  Certified when P1 surely completes and every other
+// possible cell is more than the FP32 energy bound 2 dE above it (the full
+// scan's margin); otherwise oracle_decide_t decides.
+template <class Tile>
+__device__ __forceinline__ bool oracle_fast_min_energy(const DevTable& T, const float4* __restrict__ sA,
+                                                       const float4* __restrict__ sB, const int2* __restrict__ sCol,
+                                                       const Tile& tile, const OrCtx& o, Decision& d) {
+  const int W = Tile::num_threads();
+  const int lane = tile.thread_rank();
+  const int P = T.n_powers;
+  const int n_rows = P > 0 ? T.n_trad / P : 0;
+  const float mgH = -o.ghi * kPenH;
+  float p1 = kInfF, p2 = kInfF;
+  int bi = -1;
+  auto push = [&](float key, int c) {
+    if (key < p1) bi = c;
+    p2 = fminf(p2, fmaxf(p1, key));
+    p1 = fminf(p1, key);
+  };
+  for (int r = 0; r < n_rows; ++r) {
+    const int c0 = r * P;
+    if (cell_rank_a(sB[c0]) >= o.rank_q) continue;  // the DNN's accuracy fails q_goal: no cell can be feasible
+    for (int j = lane; j < P; j += W) {
+      const int c = c0 + j;
+      const float4 A = sA[c];
+      const float x = o.sf * sB[c].x;
+      const float cap = A.y * A.x;  // (cap t) * (1/t), as or_cell
+      const float E = fmaf(cap - o.idle_f, fminf(x + o.oh, o.P), o.idleP);
+      push(pack_key(fmaxf(E, fmaf(x, kPenH, mgH)), (unsigned)c & 7u), c);
+    }
+  }
+  for (int col = lane; col < T.n_any_cols; col += W) {
+    const int2 cd = sCol[col];
+    OrRun run{false, false, 0};
+    for (int k = 0; k < cd.y; ++k) {
+      float E;
+      int rank;
+      bool met, poison;
+      or_cell(o, sA[cd.x + k], sB[cd.x + k], run, E, rank, met, poison);
+      const bool possible = poison || (met && rank < o.rank_q);
+      push(possible ? pack_key(E, (unsigned)(cd.x + k) & 7u) : kInfF, cd.x + k);
+    }
+  }
+#pragma unroll
+  for (int m = 1; m < W; m <<= 1) {
+    const float o1 = tile.shfl_xor(p1, m), o2 = tile.shfl_xor(p2, m);
+    const int ob = tile.shfl_xor(bi, m);
+    p2 = fmin3(p2, o2, fmaxf(p1, o1));
+    if (o1 < p1 || (o1 == p1 && (unsigned)ob < (unsigned)bi)) bi = ob;
+    p1 = fminf(p1, o1);
+  }
+  // margin: the FP32 energy bound of both keys (2 dE) and their 3-bit packing (< 8 ulp each)
+  if (!(p1 < kInfF) || bi < 0 || !(p2 * (1.0f - 16.0f * kEps) > p1 + 2.0f * o.dE)) return false;
+  // P1 must surely complete (and, anytime, surely deliver >= q_goal)
+  if (bi < T.n_trad) {
+    if (!(o.sf * sB[bi].x < o.glo)) return false;
+  } else {
+    const int st = cell_stage(sB[bi]);
+    OrRun run{false, false, 0};
+    float E;
+    int rank;
+    bool met = false, poison = true;
+    for (int c = bi - (st - 1); c <= bi; ++c) or_cell(o, sA[c], sB[c], run, E, rank, met, poison);
+    if (poison || !met || rank >= o.rank_q) return false;
+  }
+  d.cell = bi;
+  d.level = 0;
+  d.refined = false;
+  return true;
+}
+
 template <class Tile>
 __device__ __forceinline__ Decision oracle_decide(const DevTable& T, const float4* sA, const float4* sB,
                                                   const Cell64* C, const int2* sCol, const Tile& tile,
                                                   const SpecDev* sp, double s, double idle, double goal,
-                                                  bool fp64_all) {
+                                                  bool fp64_all, bool fast_off = false) {
   if (fp64_all) return oracle_decide_exact(T, sB, C, sCol, tile, sp, s, idle, goal);
   OrCtx o;
   make_or_ctx(o, T, sp, s, idle, goal);
   if (!(o.P > 0.0f) || !isfinite(o.dE)) return oracle_decide_exact(T, sB, C, sCol, tile, sp, s, idle, goal);
   if (sp->mode == ALERT_MODE_MAX_ACCURACY) return oracle_decide_t<1>(T, sA, sB, C, sCol, tile, sp, o);
+  if (!fast_off) {
+    const unsigned am = __activemask();
+    Decision d{-1, 0, false};
+    const bool ok = oracle_fast_min_energy(T, sA, sB, sCol, tile, o, d);
+    __syncwarp(am);
+    if (ok) return d;
+  }
   return oracle_decide_t<0>(T, sA, sB, C, sCol, tile, sp, o);
 }
 

@@ -4,6 +4,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
 #include "alert_device.cuh"
 
 namespace alert {
@@ -27,6 +31,8 @@ struct RunParams {
   int kinds;
   int c64_smem, ratio_smem, sv_smem;  // staging decisions (host computed)
   int min_energy_only;                 // every spec minimises energy: MS_MIN_ENERGY kernel
+  int any_min_energy;                  // some spec minimises energy (per-tile z-threshold slots needed)
+  int spec_shared;                     // all specs staged once per block (few specs), not per tile
   // min-energy fast scan: per (spec, traditional DNN) z-thresholds, row
   // stride n_tdnn + 1 (last = pr_threshold bound), from zlo_kernel; null = off
   const float* zlo;
@@ -34,6 +40,9 @@ struct RunParams {
   int fast_rows;  // fast scan in row mode (large tables): no staged rows / thresholds
   int units_smem; // max-accuracy fast scan: bound-sorted units staged in shared memory
   long long stream_begin, stream_end, step_begin, step_end;
+  // persistent scheduling: warps claim the next 32 / W streams from this
+  // counter (zeroed per launch) as they finish; null = static grid stride
+  unsigned long long* work;
   // Idle-filter gains (estimator.py:123-125) do not depend on the data: the
   // sequence M_k (state after k updates from m0) and W_k reaches an exact FP64
   // fixed point at k = idle_fix; M/W are precomputed on the host with the
@@ -78,11 +87,11 @@ struct SmemLayout {
     ratio = up16(c64 + sizeof(Cell64) * (size_t)n_c64);
     agg = up16(ratio + sizeof(double) * (size_t)n_tiles * (size_t)n_ratio);
     sv = up16(agg + agg_bytes * (size_t)n_tiles);
-    fz = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);  // 2 x [n_fz][n_tiles]: Z, T
-    ff = up16(fz + 2 * sizeof(float) * (size_t)n_tiles * (size_t)n_fz);  // fast-scan traditional cells
+    fz = up16(sv + sizeof(float) * (size_t)n_tiles * (size_t)n_sv);  // [n_fz][n_tiles]: the tiles' z' copies
+    ff = up16(fz + sizeof(float) * (size_t)n_tiles * (size_t)n_fz);  // fast-scan traditional cells
     wst = up16(ff + (flat ? sizeof(float4) * (size_t)(n_ff + pad_rows(W)) : 0));
     un = up16(wst + (flat ? sizeof(unsigned) * (size_t)(n_cells / 32 + 2) : 0));  // sequence, units, lbs
-    cold = up16(un + (sizeof(float4) + sizeof(int2)) * (size_t)n_sq + (sizeof(int2) + sizeof(float)) * (size_t)n_un);
+    cold = up16(un + 2 * sizeof(float4) * (size_t)n_sq + (sizeof(int2) + sizeof(float)) * (size_t)n_un);
     slot = up16(cold + sizeof(ColdState) * (size_t)n_tiles * (size_t)W);
     total = up16(slot + 16 * (size_t)n_tiles * (size_t)W);  // two 8-byte trace slots per thread
   }
@@ -124,10 +133,12 @@ __device__ __forceinline__ void prefetch_s(unsigned dst, const char* src, bool f
 struct TileAgg {
   double e, ec, a, ac;      // overall energy / delivered accuracy
   double pe, pec, pa, pac;  // current phase (loaded / stored at segment changes)
-  double oe, oec, oa, oac;  // oracle alongside
   int dn, dvl, dva, dve;    // current segment counts
-  int l1, l2, ref, osame;   // launch totals
-  int ovl, ova, ove, full;
+  int l1, l2, ref, full;    // launch totals
+};
+struct TileAggOr : TileAgg {  // + the oracle alongside (PF_BOTH kernels only)
+  double oe, oec, oa, oac;
+  int ovl, ova, ove, osame;
 };
 
 enum { PF_ALERT = 0, PF_ORACLE = 1, PF_BOTH = 2 };  // policy families
@@ -160,6 +171,7 @@ __device__ __forceinline__ void open_segment(TileAgg& g, const double* agg, int 
 // lanes of the tile split the powers.
 template <class Tile>
 __device__ __forceinline__ void fill_ratios(const DevTable& T, const Tile& tile, double* r, double idle) {
+  tile.sync();  // every lane is done reading the previous segment's ratios (racecheck)
   for (int j = tile.thread_rank(); j < T.n_powers; j += Tile::num_threads())
     r[j] = py_min(1.0, xdiv(idle, T.power_cap64[j]));
   tile.sync();
@@ -173,16 +185,20 @@ __device__ __forceinline__ void fill_ratios(const DevTable& T, const Tile& tile,
 #ifndef ALERT_MINE_REGS
 #define ALERT_MINE_REGS 128
 #endif
+#ifndef ALERT_ALL_REGS
+#define ALERT_ALL_REGS 128
+#endif
 template <int W, int PF, int MS>
-__global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_MINE_REGS : 128)
+__global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_MINE_REGS : ALERT_ALL_REGS)
     run_kernel(const RunParams P) {
   extern __shared__ float4 smem[];
   const DevTable& T = P.T;
   const int n_tiles = blockDim.x / W;
   const int n_tdnn = T.n_trad / T.n_powers;
-  const SmemLayout L(T.n_cells, T.n_any_cols, n_tiles, P.c64_smem ? T.n_cells : 0, n_tiles,
-                     P.ratio_smem ? T.n_powers : 0, sizeof(TileAgg), P.sv_smem ? T.n_cells : 0, W,
-                     (P.zlo && !P.fast_rows) ? n_tdnn : 0, (P.zlo && !P.fast_rows) ? T.n_trad : 0,
+  using Agg = typename std::conditional<PF == PF_BOTH, TileAggOr, TileAgg>::type;
+  const SmemLayout L(T.n_cells, T.n_any_cols, P.spec_shared ? P.n_specs : n_tiles, P.c64_smem ? T.n_cells : 0,
+                     n_tiles, P.ratio_smem ? T.n_powers : 0, sizeof(Agg), P.sv_smem ? T.n_cells : 0, W,
+                     (P.zlo && !P.fast_rows && P.any_min_energy) ? T.n_trad : 0, (P.zlo && !P.fast_rows) ? T.n_trad : 0,
                      P.zlo && !P.fast_rows, P.units_smem ? T.n_units : 0, P.units_smem ? T.n_seq : 0);
   char* base = reinterpret_cast<char*>(smem);
   float4* sA = smem;
@@ -191,7 +207,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   SpecDev* sSpec = reinterpret_cast<SpecDev*>(base + L.spec);
   Cell64* sC64 = reinterpret_cast<Cell64*>(base + L.c64);
   double* sRatio = reinterpret_cast<double*>(base + L.ratio);
-  TileAgg* sAgg = reinterpret_cast<TileAgg*>(base + L.agg);
+  Agg* sAgg = reinterpret_cast<Agg*>(base + L.agg);
+  if (P.spec_shared)  // few specs: one shared copy per block, a tile's spec is a pointer into it
+    for (int i = threadIdx.x; i < P.n_specs * (int)(sizeof(SpecDev) / 16); i += blockDim.x)
+      reinterpret_cast<float4*>(sSpec)[i] = reinterpret_cast<const float4*>(P.specs)[i];
   float* sV = reinterpret_cast<float*>(base + L.sv);
   ColdState* sCold = reinterpret_cast<ColdState*>(base + L.cold);
   load_table_smem(T, sA, sB, sCol);
@@ -206,17 +225,19 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
                           __int_as_float((i / W) & 7));
     }
   float4* sQA = reinterpret_cast<float4*>(base + L.un);
-  int2* sQM = reinterpret_cast<int2*>(sQA + (P.units_smem ? T.n_seq : 0));
-  int2* sUn = sQM + (P.units_smem ? T.n_seq : 0);
+  float4* sQM = sQA + (P.units_smem ? T.n_seq : 0);
+  int2* sUn = reinterpret_cast<int2*>(sQM + (P.units_smem ? T.n_seq : 0));
+  const int n_seq = T.n_seqk[P.kinds & 3];  // the policy's kinds sequence
   float* sLb = reinterpret_cast<float*>(sUn + (P.units_smem ? T.n_units : 0));
   if (P.units_smem) {
     for (int i = threadIdx.x; i < T.n_units; i += blockDim.x) {
       sUn[i] = T.units[i];
       sLb[i] = T.unit_lb[i];
     }
-    for (int i = threadIdx.x; i < T.n_seq; i += blockDim.x) {
-      sQA[i] = T.useqA[i];
-      sQM[i] = T.useqM[i];
+    const int off = ((P.kinds & 3) - 1) * T.n_seq;
+    for (int i = threadIdx.x; i < n_seq; i += blockDim.x) {
+      sQA[i] = T.useqA[off + i];
+      sQM[i] = T.useqM[off + i];
     }
   }
   unsigned* sWst = reinterpret_cast<unsigned*>(base + L.wst);
@@ -231,12 +252,30 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   const Cell64* C64 = P.c64_smem ? sC64 : T.c64;
 
   auto tile = cg::tiled_partition<W>(cg::this_thread_block());
-  const long long stream_ll = P.stream_begin + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;
-  if (stream_ll >= P.stream_end) return;
+  // Persistent: the grid is sized to the resident blocks (launch_persistent),
+  // the table is staged once per block, and each tile runs stream after
+  // stream: warps claim the next 32 / W streams from a per-launch counter
+  // (P.work) as they finish, or grid-stride when it is null.  The loop body
+  // is written inline (a lambda here is not always inlined: a call with a
+  // 3 KB stack frame in the oracle-alongside kernel).
+  const bool dyn = P.work != nullptr;
+  const int tw = (threadIdx.x & 31) / W;  // tile index within the warp
+  auto claim = [&]() -> long long {  // dynamic: the warp's next 32 / W streams
+    unsigned long long b = 0;
+    if ((threadIdx.x & 31) == 0) b = atomicAdd(P.work, (unsigned long long)(32 / W));
+    return (long long)__shfl_sync(0xffffffffu, b, 0);
+  };
+  const long long span = (long long)gridDim.x * (blockDim.x / W);
+  for (long long cur = dyn ? claim() : P.stream_begin + ((long long)blockIdx.x * blockDim.x + threadIdx.x) / W;;
+       cur = dyn ? claim() : cur + span) {
+  // dynamic: the warp stops together once its claim starts past the end
+  const long long stream_ll = dyn ? P.stream_begin + cur + tw : cur;
+  if (dyn ? P.stream_begin + cur >= P.stream_end : stream_ll >= P.stream_end) break;
+  if (stream_ll >= P.stream_end) continue;  // the claim's last warp: tiles past the end idle
   const int stream = (int)stream_ll;  // < 2^31 (checked on the host)
   const bool writer = tile.thread_rank() == 0;
   const int tid = threadIdx.x / W;  // tile index in the block
-  TileAgg& G = sAgg[tid];
+  Agg& G = sAgg[tid];
   // Cold per-stream state (group budget, segment cursor, idle power) lives in
   // the thread's shared slots, not in registers across the step loop: the
   // step loop's register budget goes to the scan.
@@ -256,15 +295,20 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   // reads are then shared-memory loads); again at every goal change.
   // min-energy fast scan: the spec's z-thresholds, copied into the tile's
   // interleaved shared slots (element d at [d * n_tiles + tile])
-  SpecDev* spec = sSpec + tid;
+  const SpecDev* spec = sSpec + tid;
   bool fast = false, fast_me = false;
   float zpr = -kInfF;
   auto stage_spec = [&](int si) {
-    const float4* src = reinterpret_cast<const float4*>(P.specs + si);
-    float4* dst = reinterpret_cast<float4*>(spec);
-    tile.sync();  // every lane is done with the previous spec
-    for (int k = tile.thread_rank(); k < (int)(sizeof(SpecDev) / 16); k += W) dst[k] = src[k];
-    tile.sync();
+    if (P.spec_shared) {
+      spec = sSpec + si;
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(P.specs + si);
+      float4* dst = reinterpret_cast<float4*>(sSpec + tid);
+      tile.sync();  // every lane is done with the previous spec
+      for (int k = tile.thread_rank(); k < (int)(sizeof(SpecDev) / 16); k += W) dst[k] = src[k];
+      tile.sync();
+      spec = sSpec + tid;
+    }
     fast = P.zlo && (spec->mode == ALERT_MODE_MIN_ENERGY || T.units);
     fast_me = fast && spec->mode == ALERT_MODE_MIN_ENERGY;  // per-DNN thresholds needed
     zpr = -kInfF;
@@ -273,28 +317,43 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       zpr = zrow[n_tdnn];
       if (!P.fast_rows && fast_me) {
         float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
-        for (int d = tile.thread_rank(); d < n_tdnn; d += W) fzZ[d * n_tiles] = zrow[d];
+        // one copy per traditional cell (not per DNN): the scan's threshold
+        // address does not depend on the cell row it loads
+        for (int c = tile.thread_rank(); c < T.n_trad; c += W) fzZ[c * n_tiles] = zrow[c / T.n_powers];
         if (W > 1) tile.sync();
       }
     }
   };
   stage_spec(cs.si);
 
+  // ALERT_FLAG_FRESH: slowdown_init / idle_power_init (estimator.py:47-56,
+  // policies.py:90-91) here instead of reading alert_state_init's arrays
+  const bool fresh = P.flags & ALERT_FLAG_FRESH;
   Filter f;
-  f.mu = P.st.mu[stream];
-  f.sigma2 = P.st.sigma2[stream];
-  f.k_gain = P.st.k_gain[stream];
-  f.q_noise = P.st.q_noise[stream];
-  f.innov = P.st.innov[stream];
-  f.phi = P.st.phi[stream];
-  f.m_var = P.st.m_var[stream];
+  if (fresh) {
+    f.mu = P.cfg.mu0;
+    f.sigma2 = P.cfg.sigma2_0;
+    f.k_gain = P.cfg.k0;
+    f.q_noise = P.cfg.q0;
+    f.innov = 0.0;
+    f.phi = T.phi0;
+    f.m_var = P.cfg.m0;
+  } else {
+    f.mu = P.st.mu[stream];
+    f.sigma2 = P.st.sigma2[stream];
+    f.k_gain = P.st.k_gain[stream];
+    f.q_noise = P.st.q_noise[stream];
+    f.innov = P.st.innov[stream];
+    f.phi = P.st.phi[stream];
+    f.m_var = P.st.m_var[stream];
+  }
   bool k_valid = false;  // k_gain == sigma2 / (sigma2 + r) holds after one update here
   int ik = -1;           // position in the idle-filter gain table
   if (P.idle_fix >= 0)
     for (int k = 0; k <= P.idle_fix; ++k)
       if (P.idle_m[k] == f.m_var) { ik = k; break; }
-  cs.budget = P.st.group_budget[stream];
-  cs.count = P.st.group_count[stream];
+  cs.budget = fresh ? 0.0 : P.st.group_budget[stream];
+  cs.count = fresh ? 0 : P.st.group_count[stream];
 
   // segment (phase) tracking; only cur_end stays in a register
   {
@@ -313,11 +372,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
 
   const bool has_agg = P.out.agg != nullptr;
   if (writer && has_agg) {
-    const double* agg = P.out.agg + stream_ll * ALERT_AGG_FIELDS;
-    G = TileAgg{};
+    double* agg = P.out.agg + stream_ll * ALERT_AGG_FIELDS;
+    if (fresh)  // written from zero: the block is never read from DRAM
+      for (int k = 0; k < ALERT_AGG_FIELDS; ++k) agg[k] = 0.0;
+    G = Agg{};
     G.e = agg[ALERT_AGG_ENERGY]; G.ec = agg[ALERT_AGG_ENERGY_C];
     G.a = agg[ALERT_AGG_ACC]; G.ac = agg[ALERT_AGG_ACC_C];
-    if (PF == PF_BOTH) {
+    if constexpr (PF == PF_BOTH) {
       G.oe = agg[ALERT_AGG_OR_ENERGY]; G.oec = agg[ALERT_AGG_OR_ENERGY_C];
       G.oa = agg[ALERT_AGG_OR_ACC]; G.oac = agg[ALERT_AGG_OR_ACC_C];
     }
@@ -387,7 +448,8 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
     double s;  // true slow-down of this input: consumed only after the decision
     if (PF == PF_ORACLE) {
       s = s_of_raw(tr, s_raw);
-      d = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, cs.idle, goal, P.flags & ALERT_FLAG_FP64_ALL);
+      d = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, cs.idle, goal, P.flags & ALERT_FLAG_FP64_ALL,
+                         P.flags & (ALERT_FLAG_NO_FAST | ALERT_FLAG_NO_ORACLE_FAST));
     } else {
       StepCtx x;
       make_ctx(x, spec, C64, f.mu, f.sigma2, f.phi, goal, P.flags & ALERT_FLAG_FP64_ALL);
@@ -401,9 +463,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
         if (P.units_smem) {
           x.su = sUn;
           x.slb = sLb;
-          if (T.n_seq) {
+          if (n_seq) {
             x.sqA = sQA;
             x.sqM = sQM;
+            x.n_seq = n_seq;
           }
         }
         float* fzZ = reinterpret_cast<float*>(base + L.fz) + tid;
@@ -468,9 +531,10 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       G.full += d.full;
     }
     if (PF == PF_BOTH) {  // OraclePolicy alongside on the same step
-      Decision od = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, idle, goal, P.flags & ALERT_FLAG_FP64_ALL);
+      Decision od = oracle_decide(T, sA, sB, C64, sCol, tile, spec, s, idle, goal, P.flags & ALERT_FLAG_FP64_ALL,
+                         P.flags & (ALERT_FLAG_NO_FAST | ALERT_FLAG_NO_ORACLE_FAST));
       const Outcome oo = execute_measure(sB, C64, spec, od.cell, s, goal, period, idle);
-      if (writer && has_agg) {
+      if constexpr (PF == PF_BOTH) if (writer && has_agg) {
         neumaier(G.oe, G.oec, oo.energy);
         neumaier(G.oa, G.oac, oo.delivered);
         G.ovl += oo.vl; G.ova += oo.va; G.ove += oo.ve;
@@ -481,7 +545,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
             pack_decision(cell_cand(sB[od.cell]), od.level, oo, false, cs.phase, od.level == 0);
     }
   }
-  if (!writer) return;
+  if (!writer) continue;
   P.st.mu[stream] = f.mu;
   P.st.sigma2[stream] = f.sigma2;
   P.st.k_gain[stream] = f.k_gain;
@@ -503,7 +567,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
     agg[ALERT_AGG_LEVEL2] += (double)G.l2;
     agg[ALERT_AGG_REFINED] += (double)G.ref;
     agg[ALERT_AGG_FULL_SCAN] += (double)G.full;
-    if (PF == PF_BOTH) {
+    if constexpr (PF == PF_BOTH) {
       agg[ALERT_AGG_OR_ENERGY] = G.oe; agg[ALERT_AGG_OR_ENERGY_C] = G.oec;
       agg[ALERT_AGG_OR_ACC] = G.oa; agg[ALERT_AGG_OR_ACC_C] = G.oac;
       agg[ALERT_AGG_OR_VIOL_LAT] += (double)G.ovl;
@@ -512,6 +576,7 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       agg[ALERT_AGG_OR_SAME] += (double)G.osame;
     }
   }
+  }  // stream loop
 }
 
 struct StepParams {
@@ -596,25 +661,38 @@ inline cudaError_t set_smem(K kern, size_t smem) {
   return cudaSuccess;
 }
 
+// Persistent launch of run_kernel: as many blocks as are resident at once
+// (occupancy x SMs, at most one per tile group of streams); the blocks
+// grid-stride over the streams.
+template <class K>
+inline cudaError_t launch_persistent(K kern, const RunParams& P, long long blocks, int tpb, size_t smem,
+                                     cudaStream_t st) {
+  cudaError_t e;
+  if ((e = set_smem(kern, smem))) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) || (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) ||
+      (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tpb, smem)))
+    return e;
+  const long long resident = (long long)std::max(1, per_sm) * std::max(1, sms);
+  // A/B knobs: ALERT_NO_PERSIST (one tile group per block), ALERT_STATIC_PERSIST (grid stride)
+  static const bool no_persist = std::getenv("ALERT_NO_PERSIST") != nullptr;
+  static const bool static_persist = std::getenv("ALERT_STATIC_PERSIST") != nullptr;
+  RunParams Q = P;
+  if (no_persist || static_persist || blocks <= resident) Q.work = nullptr;
+  else if (Q.work && (e = cudaMemsetAsync(Q.work, 0, sizeof(unsigned long long), st))) return e;
+  kern<<<(unsigned)(no_persist ? blocks : std::min(blocks, resident)), tpb, smem, st>>>(Q);
+  return cudaGetLastError();
+}
+
 #define ALERT_INSTANTIATE(W)                                                                          \
   template <>                                                                                         \
   cudaError_t launch_run<W>(int pf, const RunParams& P, int tpb, size_t smem, cudaStream_t st) {      \
-    long long blocks = ((P.stream_end - P.stream_begin) * W + tpb - 1) / tpb;                        \
-    cudaError_t e;                                                                                    \
-    if (pf == PF_ORACLE) {                                                                            \
-      if ((e = set_smem(run_kernel<W, PF_ORACLE, MS_ALL>, smem))) return e;                           \
-      run_kernel<W, PF_ORACLE, MS_ALL><<<(unsigned)blocks, tpb, smem, st>>>(P);                       \
-    } else if (pf == PF_BOTH) {                                                                       \
-      if ((e = set_smem(run_kernel<W, PF_BOTH, MS_ALL>, smem))) return e;                             \
-      run_kernel<W, PF_BOTH, MS_ALL><<<(unsigned)blocks, tpb, smem, st>>>(P);                         \
-    } else if (P.min_energy_only) {                                                                   \
-      if ((e = set_smem(run_kernel<W, PF_ALERT, MS_MIN_ENERGY>, smem))) return e;                     \
-      run_kernel<W, PF_ALERT, MS_MIN_ENERGY><<<(unsigned)blocks, tpb, smem, st>>>(P);                 \
-    } else {                                                                                          \
-      if ((e = set_smem(run_kernel<W, PF_ALERT, MS_ALL>, smem))) return e;                            \
-      run_kernel<W, PF_ALERT, MS_ALL><<<(unsigned)blocks, tpb, smem, st>>>(P);                        \
-    }                                                                                                 \
-    return cudaGetLastError();                                                                        \
+    const long long blocks = ((P.stream_end - P.stream_begin) * W + tpb - 1) / tpb;                  \
+    if (pf == PF_ORACLE) return launch_persistent(run_kernel<W, PF_ORACLE, MS_ALL>, P, blocks, tpb, smem, st); \
+    if (pf == PF_BOTH) return launch_persistent(run_kernel<W, PF_BOTH, MS_ALL>, P, blocks, tpb, smem, st); \
+    if (P.min_energy_only)                                                                            \
+      return launch_persistent(run_kernel<W, PF_ALERT, MS_MIN_ENERGY>, P, blocks, tpb, smem, st);     \
+    return launch_persistent(run_kernel<W, PF_ALERT, MS_ALL>, P, blocks, tpb, smem, st);              \
   }                                                                                                   \
   template <>                                                                                         \
   cudaError_t launch_decide<W>(const StepParams& P, uint32_t* out, int tpb, size_t smem, cudaStream_t st) { \

@@ -172,10 +172,14 @@ class Engine:
             tr = tr.with_goal_changes(packed.goal_n, packed.goal_end, packed.goal_spec)
         return tr
 
-    def new_state(self, table: GpuTable, n: int, kalman=None, idle_cfg=None, stream=None) -> dict:
+    def new_state(self, table: GpuTable, n: int, kalman=None, idle_cfg=None, stream=None, init: bool = True) -> dict:
+        """Filter state of n streams (alert_state_init).  init=False only
+        allocates: for a first alert_run with FLAG_FRESH, which initialises it."""
         torch = _torch()
         st = {k: torch.empty(n, dtype=torch.float64 if v == "f8" else torch.int32, device=self.tdev)
               for k, v in STATE_DTYPES.items()}
+        if not init:
+            return st
         cfg = filter_config(kalman, idle_cfg)
         check(load().alert_state_init(self.ctx, table.handle, C.byref(cfg), state_struct(st), n,
                                       self._stream(stream)))

@@ -130,8 +130,10 @@ def _run_batch(eng, torch, space, specs, envs, policy, kalman, idle_cfg, group_s
         launches = [(b, e, sp, torch.as_tensor(full).to(dev)) for b, e, sp, full in mode_runs(spec_arr, stream_spec)]
     else:
         launches = [(0, None, spec_arr, None)]
-    state = eng.new_state(table, ns, kalman, idle_cfg)
-    agg = torch.zeros((ns, abi.AGG_FIELDS), dtype=torch.float64, device=dev)
+    # the first step range initialises the state and zeroes the aggregates in
+    # the launch itself (FLAG_FRESH): no alert_state_init, no memset
+    state = eng.new_state(table, ns, kalman, idle_cfg, init=False)
+    agg = torch.empty((ns, abi.AGG_FIELDS), dtype=torch.float64, device=dev)
     rec = {}
     if records:
         vdt = torch.float64 if records == "f64" else torch.float32
@@ -159,8 +161,8 @@ def _run_batch(eng, torch, space, specs, envs, policy, kalman, idle_cfg, group_s
     for s0 in range(0, steps, chunk):
         for b, e, sp, ss in launches:
             eng.run(table, sp, trace, state, policy=pol, kalman=kalman, idle_cfg=idle_cfg, stream_spec=ss,
-                    outputs=out, flags=flags, stream_begin=b, stream_end=ns if e is None else e, step_begin=s0,
-                    step_end=min(steps, s0 + chunk))
+                    outputs=out, flags=flags | (abi.FLAG_FRESH if s0 == 0 else 0), stream_begin=b,
+                    stream_end=ns if e is None else e, step_begin=s0, step_end=min(steps, s0 + chunk))
     if keep_on_device:
         return BatchResult(agg, state, rec, od, table.candidates)
     torch.cuda.synchronize(dev)
@@ -243,8 +245,8 @@ class HostStreamer:
         self.copy_stream.wait_stream(comp)  # copies are ordered after the caller's prior work
         for h, dv in zip(self.map_host, self.map_dev):
             dv.copy_(h, non_blocking=True)
-        state = eng.new_state(self.table, self.n_streams, self.kalman, self.idle_cfg)
-        agg = torch.zeros((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64, device=eng.tdev)
+        state = eng.new_state(self.table, self.n_streams, self.kalman, self.idle_cfg, init=False)
+        agg = torch.empty((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64, device=eng.tdev)
         out = outputs_struct(None, agg=agg)
         stream_row = self.map_dev[1] if len(self.map_dev) > 1 else None
         copied = [torch.cuda.Event(), torch.cuda.Event()]
@@ -274,7 +276,7 @@ class HostStreamer:
             for k, (lb, le, sp) in enumerate(self.runs):
                 eng.run(self.table, sp, tr, state, policy=self.policy, kalman=self.kalman,
                         idle_cfg=self.idle_cfg, stream_spec=self.map_dev[0][k], outputs=out, stream_begin=lb,
-                        stream_end=le, step_begin=s0, step_end=s1)
+                        stream_end=le, step_begin=s0, step_end=s1, flags=abi.FLAG_FRESH if s0 == 0 else 0)
             consumed[b].record(comp)
         self.agg_host.copy_(agg, non_blocking=True)
         return self.agg_host

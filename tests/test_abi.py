@@ -49,7 +49,7 @@ def test_version_and_strerror():
     from paper_1911_00119_b200 import _lib
 
     L = _lib.load()
-    assert L.alert_abi_version() == 3
+    assert L.alert_abi_version() == 4
     assert L.alert_strerror(-3) == b"invalid constraint spec"
 
 

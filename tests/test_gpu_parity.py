@@ -472,3 +472,41 @@ def test_erfc_rel_relative_error_bound():
     ref = np.array([math.erfc(v) for v in xf])
     rel = np.abs(got / ref - 1.0)
     assert rel.max() < 5e-5, rel.max()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_oracle_fast_min_energy_equals_full(seed):
+    """The oracle's certified min-energy fast scan (accuracy-infeasible DNN
+    rows skipped, deadline as a sign-exact penalty) changes no oracle decision
+    against the full oracle scan (ALERT_FLAG_NO_FAST) and the all-FP64 oracle,
+    for the oracle alone and fused alongside ALERT, at one and eight lanes per
+    stream; constant slow-down phases put completions on the deadline band."""
+    rnd = random.Random(7171 + seed)
+    space = random_space(rnd, 8, 8) if seed % 2 else A.preset_space()
+    specs = _min_energy_specs(rnd, space)
+    envs = []
+    for k in range(24):
+        phases = (A.EnvironmentPhase(50, A.Constant(rnd.uniform(0.5, 1.5)), rnd.uniform(1, 9), 0.0),
+                  A.EnvironmentPhase(50, A.LogNormal(rnd.uniform(-0.2, 0.7), 0.3), rnd.uniform(1, 9), 0.05))
+        envs.append(A.realize(A.Trace(seed=rnd.randint(0, 2**31), phases=phases)))
+    lanes = [1, 8][seed % 2]
+    for policy in ("oracle", "alert+oracle"):
+        fast = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64, lanes_per_stream=lanes)
+        full = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64, lanes_per_stream=lanes,
+                           flags=abi.FLAG_NO_FAST)
+        exact = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64,
+                            lanes_per_stream=lanes, flags=abi.FLAG_FP64_ALL)
+        if policy == "oracle":
+            np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
+            np.testing.assert_array_equal(fast.decoded()["cand"], exact.decoded()["cand"])
+        else:
+            np.testing.assert_array_equal(fast.oracle_decision & 0xFFFF, full.oracle_decision & 0xFFFF)
+            np.testing.assert_array_equal(fast.oracle_decision & 0xFFFF, exact.oracle_decision & 0xFFFF)
+        np.testing.assert_array_equal(fast.agg[:, abi.AGG_OR_ENERGY:abi.AGG_FULL_SCAN],
+                                      full.agg[:, abi.AGG_OR_ENERGY:abi.AGG_FULL_SCAN])
+    A.get_engine().set_launch(0, 0)
+    for k in range(0, len(envs), 6):  # the CPU oracle (reference restatement) picks the same
+        rec, _, _ = oracle.run(space, specs[k % len(specs)], envs[k], "oracle")
+        own = A.run_batch(space, [specs[k % len(specs)]], [envs[k]], "oracle", records="f64",
+                          trace_dtype=np.float64)
+        np.testing.assert_array_equal(own.decoded()["cand"][:, 0], rec["cand"])
