@@ -26,7 +26,7 @@ def launches(path):
         v = float(r[idx["Metric Value"]].replace(",", ""))
         unit = r[idx["Metric Unit"]]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3, "second": 1}.get(unit, 1)
+                 "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1}.get(unit, 1)
         d[r[idx["Metric Name"]]] = v * scale
     return list(out.values())
 
