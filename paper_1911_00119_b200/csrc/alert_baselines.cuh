@@ -214,16 +214,16 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
   if (agg) {
     G.e = agg[ALERT_AGG_ENERGY]; G.ec = agg[ALERT_AGG_ENERGY_C];
     G.a = agg[ALERT_AGG_ACC]; G.ac = agg[ALERT_AGG_ACC_C];
-    open_segment(G, agg, phase);
+    open_segment(G, agg, phase, false);
   }
   for (long long n = P.step_begin; n < P.step_end; ++n) {
     if (n >= cur_end) {
-      if (agg) flush_segment(G, agg, phase);
+      if (agg) flush_segment(G, agg, phase, false);
       while (seg + 1 < nseg && n >= tr.seg_end[seg0 + seg]) ++seg;
       cur_end = seg + 1 < nseg ? tr.seg_end[seg0 + seg] : 0x7fffffff;
       phase = tr.seg_phase[seg0 + seg];
       idle = tr.seg_idle[seg0 + seg];
-      if (agg) open_segment(G, agg, phase);
+      if (agg) open_segment(G, agg, phase, false);
     }
     if (n >= gend) {  // goal change (policy.spec swapped)
       gseg = goal_seek(tr, gseg0, ng, gseg, n);
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(128) baseline_kernel(const BaseParams P) {
   P.st.group_count[stream] = count;
   if (P.st.policy_aux) P.st.policy_aux[stream] = aux;
   if (agg) {
-    flush_segment(G, agg, phase);
+    flush_segment(G, agg, phase, false);
     const double steps = (double)(P.step_end - P.step_begin);
     agg[ALERT_AGG_N] += steps;
     agg[ALERT_AGG_ENERGY] = G.e; agg[ALERT_AGG_ENERGY_C] = G.ec;

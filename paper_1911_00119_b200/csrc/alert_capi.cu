@@ -599,6 +599,29 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     }
     std::stable_sort(trows.begin(), trows.end(), [](const float4& a, const float4& b) { return a.y < b.y; });
   }
+  // oracle max-accuracy fast scan: traditional DNN rows {first cell, rank of
+  // the DNN's accuracy, smallest FP32 latency of the row, 0} by rank, best first
+  std::vector<float4> orows;
+  if (P > 0 && !trad_cells.empty()) {
+    for (int dn = 0; dn < (int)trad_cells.size() / P; ++dn) {
+      float tmin = B[(size_t)dn * P].x;
+      for (int j = 1; j < P; ++j) tmin = std::min(tmin, B[(size_t)dn * P + j].x);
+      uint32_t rk;
+      memcpy(&rk, &B[(size_t)dn * P].w, 4);
+      const int first = dn * P, rank = (int)(rk & 0xFFFF);
+      float ff, rf;
+      memcpy(&ff, &first, 4);
+      memcpy(&rf, &rank, 4);
+      orows.push_back(make_float4(ff, rf, tmin, 0.0f));
+    }
+    std::stable_sort(orows.begin(), orows.end(), [](const float4& a, const float4& b) {
+      int ra, rb;
+      memcpy(&ra, &a.y, 4);
+      memcpy(&rb, &b.y, 4);
+      return ra < rb;
+    });
+  }
+  size_t oOrows = place(sizeof(float4) * orows.size());
   size_t oTrows = place(sizeof(float4) * trows.size());
   size_t oUnit = place(sizeof(int2) * units.size()), oUlb = place(4 * units.size());
   size_t oSeqA = place(sizeof(float4) * 3 * n_seq), oSeqM = place(sizeof(float4) * 3 * n_seq);
@@ -634,6 +657,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
     memcpy(&h[oUlb], unit_lb.data(), 4 * units.size());
   }
   if (!trows.empty()) memcpy(&h[oTrows], trows.data(), sizeof(float4) * trows.size());
+  if (!orows.empty()) memcpy(&h[oOrows], orows.data(), sizeof(float4) * orows.size());
   for (int v = 0; v < 3; ++v)
     if (!seqM[v].empty()) {
       memcpy(&h[oSeqA + sizeof(float4) * v * n_seq], seqA[v].data(), sizeof(float4) * seqA[v].size());
@@ -669,6 +693,7 @@ int alert_table_create(AlertContext* ctx, const AlertSpaceDesc* d, AlertTable** 
   T.n_seqk[0] = 0;
   for (int v = 0; v < 3; ++v) T.n_seqk[v + 1] = (int)seqM[v].size();
   T.trad_rows = trows.empty() ? nullptr : reinterpret_cast<const float4*>(buf + oTrows);
+  T.or_rows = orows.empty() ? nullptr : reinterpret_cast<const float4*>(buf + oOrows);
   T.app_first = app_stages > 0 ? reinterpret_cast<const int*>(buf + oApp) : nullptr;
   T.app_stages = app_stages;
   T.cap_max = (float)max_cap;
@@ -765,7 +790,8 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
       (P.fast_rows || !any_min_energy || (size_t)(tpb / W) * (size_t)T.n_trad * sizeof(float) <= 16 * 1024))
     P.fast_smem = 1;  // alert_run computes the thresholds (zlo_kernel) and sets P.zlo
   // max-accuracy fast scan needs its sorted units in shared memory
-  if (P.fast_smem && any_max_accuracy && T.units && T.n_units <= 1024) P.units_smem = 1;
+  // (alert_run drops the staging again if the block's shared memory exceeds the limit)
+  if (P.fast_smem && any_max_accuracy && T.units && T.n_units <= 4096) P.units_smem = 1;
   P.c64_smem = T.n_cells <= kC64SmemMax;
   P.ratio_smem = T.n_powers <= kRatioSmemMax &&
                  (size_t)(tpb / W) * (size_t)T.n_powers * sizeof(double) <= 16 * 1024;
@@ -779,6 +805,10 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
   const bool flat = W == 1 && T.n_seq > 0 && P.units_smem;
   P.sv_smem = refine_heavy && !flat && (size_t)(tpb / W) * (size_t)T.n_cells * sizeof(float) <= 32 * 1024;
 }
+
+// the flat W = 1 max-accuracy scan needs its staged sequence; larger unit
+// tables can be read through L1 when shared memory is short
+static bool T_units_large(const AlertTable* tb) { return tb->dev.n_seq == 0; }
 
 static size_t run_smem(const AlertTable* tb, int n_specs, int tpb, int W, const RunParams& P) {
   const DevTable& T = tb->dev;
@@ -999,6 +1029,10 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   auto stage = [&](int tpb) {
     run_staging(tb, specs, n_specs, tpb, W, P, policy, flags);
     size_t sm = run_smem(tb, n_specs, tpb, W, P);
+    if ((int)sm > ctx->max_smem && P.units_smem && T_units_large(tb)) {  // units read through L1 instead
+      P.units_smem = 0;
+      sm = run_smem(tb, n_specs, tpb, W, P);
+    }
     if ((int)sm > ctx->max_smem && P.fast_smem) {  // no room for the fast-scan tables
       P.fast_smem = 0;
       sm = run_smem(tb, n_specs, tpb, W, P);

@@ -66,6 +66,7 @@ struct DevTable {
   int n_seq;       // the longest sequence (shared-memory slots)
   int n_seqk[4];   // length per kinds (index 1..3)
   const float4* trad_rows;  // min-energy row mode: {dnn bits, min cap * t, max 1/t, 0}, min cap * t ascending
+  const float4* or_rows;    // oracle max-accuracy: {first cell bits, accuracy rank bits, min t, 0}, rank ascending
   float cap_min;            // smallest cap (FP32)
 
   const int* sys_cells;   // [n_powers] or null
@@ -971,10 +972,30 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
   // pass, which then re-derives only the tails of the few tied cells.
   const bool store = W == 1 && x.has_sv;
   int u_end = lane;
-  for (int u = lane; u < n_units; u += W) {
-    if (lb_at(u) >= t.p2) break;
+  // the next unit and its bound are loaded one iteration ahead (their
+  // latency hides behind the current unit); at W > 1 the lanes stop on the
+  // tile's smallest P2 (a lane holding two keys <= lb already excludes every
+  // later unit from the tile's top 2), shared every iteration
+  float lb_n = lane < n_units ? lb_at(lane) : kInfF;
+  int2 un_n = lane < n_units ? unit_at(lane) : make_int2(0, 0);
+  // (the tile iterates together until every lane is done: bounds only grow
+  // along the sorted units and the tile's P2 only falls, so a lane stays done)
+  for (int u = lane;; u += W) {
+    const float lb = lb_n;
+    const int2 un = un_n;
+    if (u + W < n_units) {
+      lb_n = lb_at(u + W);
+      un_n = unit_at(u + W);
+    }
+    float p2_tile = t.p2;
+    if (W > 1) {
+#pragma unroll
+      for (int o = 1; o < W; o <<= 1) p2_tile = fminf(p2_tile, tile.shfl_xor(p2_tile, o));
+    }
+    const bool done = u >= n_units || lb >= p2_tile;
+    if (W > 1 ? tile.all(done) : done) break;
+    if (done) continue;
     u_end = u + W;
-    const int2 un = unit_at(u);
     if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
     const int n = un.y & 0xFFFF;
     float acc = sA[un.x].w;
@@ -1981,6 +2002,70 @@ __device__ __forceinline__ bool oracle_fast_min_energy(const DevTable& T, const 
   return true;
 }
 
+// OraclePolicy.decide, max-accuracy level 0 (policies.py:160-205: complete
+// and E <= e_goal, then the highest delivered accuracy, then the lowest
+// energy) with the full scan's classification and certificate, visiting
+// only the DNN rows that can matter.  Anytime columns first (their delivered
+// class varies per stage), then the traditional rows best accuracy class
+// first (T.or_rows): a completing traditional cell delivers its DNN's
+// accuracy, so once the tile holds a surely feasible cell of class r1, rows
+// of a worse class can neither beat r1 nor make it uncertain (a maybe-
+// completing cell of such a row still delivers a worse class or fails level
+// 0) and the scan stops; a row whose fastest cell surely misses the deadline
+// is skipped.  Certified as in oracle_decide_t (no uncertain cell of class
+// <= r1, the best energy of class r1 clear of the next by 2 dE); otherwise the
+// full scan decides.
+template <class Tile>
+__device__ __forceinline__ bool oracle_fast_max_accuracy(const DevTable& T, const float4* __restrict__ sA,
+                                                         const float4* __restrict__ sB,
+                                                         const int2* __restrict__ sCol, const Tile& tile,
+                                                         const OrCtx& o, Decision& d) {
+  const int W = Tile::num_threads();
+  const int lane = tile.thread_rank();
+  const int P = T.n_powers;
+  const int n_rows = P > 0 ? T.n_trad / P : 0;
+  LexTracker lx;
+  lx.init();
+  for (int col = lane; col < T.n_any_cols; col += W) {
+    const int2 cd = sCol[col];
+    OrRun run{false, false, 0};
+    for (int k = 0; k < cd.y; ++k) {
+      float E;
+      int rank;
+      bool met, poison;
+      or_cell(o, sA[cd.x + k], sB[cd.x + k], run, E, rank, met, poison);
+      const bool sure = !poison && met && E <= o.e_lo;
+      const bool unc = (poison && E <= o.e_hi) || (!poison && met && E > o.e_lo && E <= o.e_hi);
+      lx.push(rank, E, sure, unc, poison ? 0 : rank, cd.x + k);
+    }
+  }
+  for (int r = 0; r < n_rows; ++r) {
+    const float4 R = __ldg(T.or_rows + r);
+    const int rank = __float_as_int(R.y);
+    if (tile.any(lx.r1 < rank)) break;             // a better class is surely feasible: no later row matters
+    if (!(o.sf * R.z <= o.ghi)) continue;          // even the fastest cell surely misses the deadline
+    const int c0 = __float_as_int(R.x);
+    for (int j = lane; j < P; j += W) {
+      const int c = c0 + j;
+      const float4 A = sA[c];
+      const float x = o.sf * sB[c].x;
+      const float cap = A.y * A.x;  // as or_cell
+      const float E = fmaf(cap - o.idle_f, fminf(x + o.oh, o.P), o.idleP);
+      const bool band = x >= o.glo && x <= o.ghi;
+      const bool done = x <= o.goal_f;
+      const bool sure = !band && done && E <= o.e_lo;
+      const bool unc = (band && E <= o.e_hi) || (!band && done && E > o.e_lo && E <= o.e_hi);
+      lx.push(rank, E, sure, unc, rank, c);  // a maybe-completing traditional cell can only deliver its DNN's class
+    }
+  }
+  lx.merge(tile);
+  if (lx.r1 == 0x7fffffff || !(lx.un > lx.r1) || !(lx.e2 > lx.e1 + 2.0f * o.dE)) return false;
+  d.cell = lx.i1;
+  d.level = 0;
+  d.refined = false;
+  return true;
+}
+
 template <class Tile>
 __device__ __forceinline__ Decision oracle_decide(const DevTable& T, const float4* sA, const float4* sB,
                                                   const Cell64* C, const int2* sCol, const Tile& tile,
@@ -1990,7 +2075,16 @@ __device__ __forceinline__ Decision oracle_decide(const DevTable& T, const float
   OrCtx o;
   make_or_ctx(o, T, sp, s, idle, goal);
   if (!(o.P > 0.0f) || !isfinite(o.dE)) return oracle_decide_exact(T, sB, C, sCol, tile, sp, s, idle, goal);
-  if (sp->mode == ALERT_MODE_MAX_ACCURACY) return oracle_decide_t<1>(T, sA, sB, C, sCol, tile, sp, o);
+  if (sp->mode == ALERT_MODE_MAX_ACCURACY) {
+    if (!fast_off && T.or_rows) {
+      const unsigned am = __activemask();
+      Decision d{-1, 0, false};
+      const bool ok = oracle_fast_max_accuracy(T, sA, sB, sCol, tile, o, d);
+      __syncwarp(am);
+      if (ok) return d;
+    }
+    return oracle_decide_t<1>(T, sA, sB, C, sCol, tile, sp, o);
+  }
   if (!fast_off) {
     const unsigned am = __activemask();
     Decision d{-1, 0, false};

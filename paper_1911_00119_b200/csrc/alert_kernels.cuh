@@ -135,6 +135,7 @@ struct TileAgg {
   double pe, pec, pa, pac;  // current phase (loaded / stored at segment changes)
   int dn, dvl, dva, dve;    // current segment counts
   int l1, l2, ref, full;    // launch totals
+  int tvl, tva, tve, seen;  // ALERT_FLAG_FRESH: violation totals, phases whose slot is written
 };
 struct TileAggOr : TileAgg {  // + the oracle alongside (PF_BOTH kernels only)
   double oe, oec, oa, oac;
@@ -146,20 +147,35 @@ enum { PF_ALERT = 0, PF_ORACLE = 1, PF_BOTH = 2 };  // policy families
 
 // Close the current segment: per-phase slot (phase ids < ALERT_MAX_PHASES) and
 // overall violation counts.
-__device__ __forceinline__ void flush_segment(TileAgg& g, double* agg, int phase) {
+// With ALERT_FLAG_FRESH the block is written, never read: a phase slot's
+// first flush stores, a recurring phase's adds to what this launch stored,
+// the overall counts stay in the tile until the end (finish_fresh).
+__device__ __forceinline__ void flush_segment(TileAgg& g, double* agg, int phase, bool fresh) {
   if (phase >= 0 && phase < ALERT_MAX_PHASES) {
     double* p = agg + ALERT_AGG_PHASE_BASE + ALERT_AGG_PHASE_STRIDE * phase;
-    p[0] += (double)g.dn;
+    if (fresh && !((g.seen >> phase) & 1)) {
+      p[0] = (double)g.dn;
+      p[5] = (double)g.dvl; p[6] = (double)g.dva; p[7] = (double)g.dve;
+      g.seen |= 1 << phase;
+    } else {
+      p[0] += (double)g.dn;
+      p[5] += (double)g.dvl; p[6] += (double)g.dva; p[7] += (double)g.dve;
+    }
     p[1] = g.pe; p[2] = g.pec; p[3] = g.pa; p[4] = g.pac;
-    p[5] += (double)g.dvl; p[6] += (double)g.dva; p[7] += (double)g.dve;
   }
-  agg[ALERT_AGG_VIOL_LAT] += (double)g.dvl;
-  agg[ALERT_AGG_VIOL_ACC] += (double)g.dva;
-  agg[ALERT_AGG_VIOL_ENERGY] += (double)g.dve;
+  if (fresh) {
+    g.tvl += g.dvl; g.tva += g.dva; g.tve += g.dve;
+  } else {
+    agg[ALERT_AGG_VIOL_LAT] += (double)g.dvl;
+    agg[ALERT_AGG_VIOL_ACC] += (double)g.dva;
+    agg[ALERT_AGG_VIOL_ENERGY] += (double)g.dve;
+  }
   g.dn = g.dvl = g.dva = g.dve = 0;
 }
-__device__ __forceinline__ void open_segment(TileAgg& g, const double* agg, int phase) {
-  if (phase >= 0 && phase < ALERT_MAX_PHASES) {
+__device__ __forceinline__ void open_segment(TileAgg& g, const double* agg, int phase, bool fresh) {
+  if (fresh && phase >= 0 && phase < ALERT_MAX_PHASES && !((g.seen >> phase) & 1)) {
+    g.pe = g.pec = g.pa = g.pac = 0.0;
+  } else if (phase >= 0 && phase < ALERT_MAX_PHASES) {
     const double* p = agg + ALERT_AGG_PHASE_BASE + ALERT_AGG_PHASE_STRIDE * phase;
     g.pe = p[1]; g.pec = p[2]; g.pa = p[3]; g.pac = p[4];
   } else {
@@ -373,16 +389,16 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   const bool has_agg = P.out.agg != nullptr;
   if (writer && has_agg) {
     double* agg = P.out.agg + stream_ll * ALERT_AGG_FIELDS;
-    if (fresh)  // written from zero: the block is never read from DRAM
-      for (int k = 0; k < ALERT_AGG_FIELDS; ++k) agg[k] = 0.0;
     G = Agg{};
-    G.e = agg[ALERT_AGG_ENERGY]; G.ec = agg[ALERT_AGG_ENERGY_C];
-    G.a = agg[ALERT_AGG_ACC]; G.ac = agg[ALERT_AGG_ACC_C];
-    if constexpr (PF == PF_BOTH) {
-      G.oe = agg[ALERT_AGG_OR_ENERGY]; G.oec = agg[ALERT_AGG_OR_ENERGY_C];
-      G.oa = agg[ALERT_AGG_OR_ACC]; G.oac = agg[ALERT_AGG_OR_ACC_C];
+    if (!fresh) {  // FRESH: the sums start at zero, the block is only written (at the end)
+      G.e = agg[ALERT_AGG_ENERGY]; G.ec = agg[ALERT_AGG_ENERGY_C];
+      G.a = agg[ALERT_AGG_ACC]; G.ac = agg[ALERT_AGG_ACC_C];
+      if constexpr (PF == PF_BOTH) {
+        G.oe = agg[ALERT_AGG_OR_ENERGY]; G.oec = agg[ALERT_AGG_OR_ENERGY_C];
+        G.oa = agg[ALERT_AGG_OR_ACC]; G.oac = agg[ALERT_AGG_OR_ACC_C];
+      }
     }
-    open_segment(G, agg, cs.phase);
+    open_segment(G, agg, cs.phase, fresh);
   }
 
   // Trace prefetch: the next step's slow-down is copied global -> shared with
@@ -410,13 +426,13 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
       const int nseg = cs.nseg;
       const long long seg0 = cs.seg0;
       if (seg + 1 < nseg && n >= tr.seg_end[seg0 + seg]) {
-        if (has_agg && writer) flush_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase);
+        if (has_agg && writer) flush_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase, fresh);
         while (seg + 1 < nseg && n >= tr.seg_end[seg0 + seg]) ++seg;
         cs.seg = seg;
         cs.phase = tr.seg_phase[seg0 + seg];
         cs.idle = tr.seg_idle[seg0 + seg];
         if (P.ratio_smem) fill_ratios(T, tile, sRatio + (size_t)tid * T.n_powers, cs.idle);
-        if (has_agg && writer) open_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase);
+        if (has_agg && writer) open_segment(G, P.out.agg + stream_ll * ALERT_AGG_FIELDS, cs.phase, fresh);
       }
       if (n >= cs.gend) {  // goal change: the row's next spec (policy.spec swapped)
         cs.gseg = goal_seek(tr, cs.gseg0, cs.ngseg, cs.gseg, n);
@@ -555,25 +571,43 @@ __global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_M
   P.st.m_var[stream] = f.m_var;
   P.st.group_budget[stream] = cs.budget;
   P.st.group_count[stream] = cs.count;
+  if (fresh && P.st.policy_aux) P.st.policy_aux[stream] = -1;  // as alert_state_init (comparison schemes only)
   if (has_agg) {
     double* agg = P.out.agg + stream_ll * ALERT_AGG_FIELDS;
-    flush_segment(G, agg, cs.phase);
+    flush_segment(G, agg, cs.phase, fresh);
     const double steps = (double)(P.step_end - P.step_begin);
-    agg[ALERT_AGG_N] += steps;
+    // counters: added to the block, or (FRESH) stored — every field written
+    // once and none read, the unvisited phase slots and the spare fields zeroed
+    auto put = [&](int k, double v) {
+      if (fresh) agg[k] = v;
+      else agg[k] += v;
+    };
+    if (fresh) {
+      agg[ALERT_AGG_VIOL_LAT] = (double)G.tvl;
+      agg[ALERT_AGG_VIOL_ACC] = (double)G.tva;
+      agg[ALERT_AGG_VIOL_ENERGY] = (double)G.tve;
+      for (int k = ALERT_AGG_FULL_SCAN + 1; k < ALERT_AGG_PHASE_BASE; ++k) agg[k] = 0.0;
+      for (int ph = 0; ph < ALERT_MAX_PHASES; ++ph)
+        if (!((G.seen >> ph) & 1))
+          for (int k = 0; k < ALERT_AGG_PHASE_STRIDE; ++k) agg[ALERT_AGG_PHASE_BASE + ALERT_AGG_PHASE_STRIDE * ph + k] = 0.0;
+    }
+    put(ALERT_AGG_N, steps);
     agg[ALERT_AGG_ENERGY] = G.e; agg[ALERT_AGG_ENERGY_C] = G.ec;
     agg[ALERT_AGG_ACC] = G.a; agg[ALERT_AGG_ACC_C] = G.ac;
-    agg[ALERT_AGG_LEVEL0] += steps - (double)G.l1 - (double)G.l2;
-    agg[ALERT_AGG_LEVEL1] += (double)G.l1;
-    agg[ALERT_AGG_LEVEL2] += (double)G.l2;
-    agg[ALERT_AGG_REFINED] += (double)G.ref;
-    agg[ALERT_AGG_FULL_SCAN] += (double)G.full;
+    put(ALERT_AGG_LEVEL0, steps - (double)G.l1 - (double)G.l2);
+    put(ALERT_AGG_LEVEL1, (double)G.l1);
+    put(ALERT_AGG_LEVEL2, (double)G.l2);
+    put(ALERT_AGG_REFINED, (double)G.ref);
+    put(ALERT_AGG_FULL_SCAN, (double)G.full);
     if constexpr (PF == PF_BOTH) {
       agg[ALERT_AGG_OR_ENERGY] = G.oe; agg[ALERT_AGG_OR_ENERGY_C] = G.oec;
       agg[ALERT_AGG_OR_ACC] = G.oa; agg[ALERT_AGG_OR_ACC_C] = G.oac;
-      agg[ALERT_AGG_OR_VIOL_LAT] += (double)G.ovl;
-      agg[ALERT_AGG_OR_VIOL_ACC] += (double)G.ova;
-      agg[ALERT_AGG_OR_VIOL_ENERGY] += (double)G.ove;
-      agg[ALERT_AGG_OR_SAME] += (double)G.osame;
+      put(ALERT_AGG_OR_VIOL_LAT, (double)G.ovl);
+      put(ALERT_AGG_OR_VIOL_ACC, (double)G.ova);
+      put(ALERT_AGG_OR_VIOL_ENERGY, (double)G.ove);
+      put(ALERT_AGG_OR_SAME, (double)G.osame);
+    } else if (fresh) {
+      for (int k = ALERT_AGG_OR_ENERGY; k <= ALERT_AGG_OR_SAME; ++k) agg[k] = 0.0;
     }
   }
   }  // stream loop

@@ -510,3 +510,95 @@ def test_oracle_fast_min_energy_equals_full(seed):
         own = A.run_batch(space, [specs[k % len(specs)]], [envs[k]], "oracle", records="f64",
                           trace_dtype=np.float64)
         np.testing.assert_array_equal(own.decoded()["cand"][:, 0], rec["cand"])
+
+
+@pytest.mark.parametrize("policy", ["alert", "alert+oracle", "sys-only"])
+def test_fresh_flag_equals_initialised_state_and_zeroed_aggregates(policy):
+    """ALERT_FLAG_FRESH (state initialised and aggregate blocks written, never
+    read, inside the launch) gives the same per-stream aggregates and final
+    state, bit for bit, as alert_state_init + a zeroed block + an
+    accumulating launch — on traces whose phases recur (a phase slot flushed
+    twice) and with goal modes mixed."""
+    import torch
+
+    from paper_1911_00119_b200.engine import outputs_struct
+    from paper_1911_00119_b200.packing import pack_specs, policy_code
+
+    rnd = random.Random(515)
+    space = random_space(rnd, 5, 5)
+    ref = A.reference_latency(space)
+    specs = [A.ConstraintSpec(mode=A.Mode.MINIMIZE_ENERGY, t_goal=ref, q_goal=0.6, overhead_budget=0.01 * ref),
+             A.ConstraintSpec(mode=A.Mode.MAXIMIZE_ACCURACY, t_goal=ref, e_goal=0.5 * space.max_power.cap_watts * ref,
+                              pr_threshold=0.9, overhead_budget=0.01 * ref)]
+    envs = []
+    for k in range(40):
+        ph = (A.EnvironmentPhase(30, A.Constant(rnd.uniform(0.7, 1.4)), rnd.uniform(2, 8), 0.02),
+              A.EnvironmentPhase(20, A.LogNormal(0.3, 0.3), rnd.uniform(2, 8), 0.05))
+        env = A.realize(A.Trace(seed=k, phases=ph))
+        # phase ids 0, 1, 0: phase 0 recurs
+        phase = np.concatenate([env.phase_index[:20], env.phase_index[30:50], np.zeros(10, np.int64)])
+        idle = np.concatenate([env.idle_power[:20], env.idle_power[30:50], env.idle_power[:10]])
+        envs.append(A.TrueEnvironment(env.slowdown, idle, phase))
+    eng = A.get_engine()
+    table = eng.table(space)
+    trace = eng.upload_trace(pack_envs(envs, dtype=np.float64))
+    spec_arr = pack_specs(specs)
+    ss = torch.as_tensor(np.arange(len(envs), dtype=np.int32) % 2).to(eng.tdev)
+    out = {}
+    for fresh in (False, True):
+        state = eng.new_state(table, len(envs), init=not fresh)
+        shape = (len(envs), abi.AGG_FIELDS)  # FRESH must overwrite whatever the block held
+        agg = (torch.full(shape, 7.0, dtype=torch.float64, device=eng.tdev) if fresh else
+               torch.zeros(shape, dtype=torch.float64, device=eng.tdev))
+        eng.run(table, spec_arr, trace, state, policy=policy_code(policy), stream_spec=ss,
+                outputs=outputs_struct(None, agg=agg), flags=abi.FLAG_FRESH if fresh else 0)
+        out[fresh] = (agg.cpu().numpy(), {k: v.cpu().numpy() for k, v in state.items()})
+    np.testing.assert_array_equal(out[True][0], out[False][0])
+    for k in out[False][1]:
+        np.testing.assert_array_equal(out[True][1][k], out[False][1][k])
+    assert out[True][0][:, abi.AGG_PHASE_BASE].sum() > 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_oracle_fast_max_accuracy_equals_full(seed):
+    """The oracle's max-accuracy fast scan (DNN rows best accuracy class
+    first, stop once a better class is surely feasible, dead rows skipped)
+    picks exactly what the full oracle scan and the all-FP64 oracle pick,
+    alone and alongside ALERT, at one and eight lanes per stream."""
+    rnd = random.Random(8282 + seed)
+    space = random_space(rnd, 8, 8) if seed % 2 else A.generate_space(A.ProfileKnobs(n_dnns=12, n_powers=6))
+    ref = A.reference_latency(space)
+    specs = []
+    for k in range(6):
+        t = ref * rnd.uniform(0.3, 2.0)
+        specs.append(A.ConstraintSpec(mode=A.Mode.MAXIMIZE_ACCURACY, t_goal=t,
+                                      e_goal=rnd.uniform(0.1, 1.0) * space.max_power.cap_watts * t,
+                                      pr_threshold=[None, 0.9][k % 2], overhead_budget=0.01 * ref))
+    envs = []
+    for k in range(24):
+        phases = (A.EnvironmentPhase(50, A.Constant(rnd.uniform(0.5, 1.5)), rnd.uniform(1, 9), 0.0),
+                  A.EnvironmentPhase(50, A.LogNormal(rnd.uniform(-0.2, 0.7), 0.3), rnd.uniform(1, 9), 0.05))
+        envs.append(A.realize(A.Trace(seed=rnd.randint(0, 2**31), phases=phases)))
+    lanes = [1, 8][seed % 2]
+    for policy in ("oracle", "alert+oracle"):
+        fast = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64, lanes_per_stream=lanes)
+        full = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64, lanes_per_stream=lanes,
+                           flags=abi.FLAG_NO_ORACLE_FAST)
+        exact = A.run_batch(space, specs, envs, policy, records="f64", trace_dtype=np.float64,
+                            lanes_per_stream=lanes, flags=abi.FLAG_FP64_ALL)
+        if policy == "oracle":
+            np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
+            np.testing.assert_array_equal(fast.decoded()["cand"], exact.decoded()["cand"])
+            np.testing.assert_array_equal(fast.agg[:, :abi.AGG_REFINED], full.agg[:, :abi.AGG_REFINED])
+            np.testing.assert_array_equal(fast.agg[:, abi.AGG_PHASE_BASE:], full.agg[:, abi.AGG_PHASE_BASE:])
+        else:
+            np.testing.assert_array_equal(fast.oracle_decision & 0xFFFF, full.oracle_decision & 0xFFFF)
+            np.testing.assert_array_equal(fast.oracle_decision & 0xFFFF, exact.oracle_decision & 0xFFFF)
+            np.testing.assert_array_equal(fast.agg[:, abi.AGG_OR_ENERGY:abi.AGG_FULL_SCAN],
+                                          full.agg[:, abi.AGG_OR_ENERGY:abi.AGG_FULL_SCAN])
+    A.get_engine().set_launch(0, 0)
+    for k in range(0, len(envs), 6):  # the CPU oracle (reference restatement) picks the same
+        rec, _, _ = oracle.run(space, specs[k % len(specs)], envs[k], "oracle")
+        own = A.run_batch(space, [specs[k % len(specs)]], [envs[k]], "oracle", records="f64",
+                          trace_dtype=np.float64)
+        np.testing.assert_array_equal(own.decoded()["cand"][:, 0], rec["cand"])
