@@ -774,6 +774,7 @@ static void run_staging(const AlertTable* tb, const AlertSpec* specs, int n_spec
   }
   P.min_energy_only = all_min_energy;
   P.any_min_energy = any_min_energy;
+  P.max_accuracy_only = !any_min_energy;
   // few specs: staged once per block (a tile's spec is a pointer), else one copy per tile
   static const bool no_shared_specs = std::getenv("ALERT_NO_SPEC_SHARED") != nullptr;  // A/B knob
   P.spec_shared = !no_shared_specs && n_specs <= kSpecSmemMax && n_specs < tpb / W;
@@ -1029,9 +1030,17 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   auto stage = [&](int tpb) {
     run_staging(tb, specs, n_specs, tpb, W, P, policy, flags);
     size_t sm = run_smem(tb, n_specs, tpb, W, P);
-    if ((int)sm > ctx->max_smem && P.units_smem && T_units_large(tb)) {  // units read through L1 instead
+    if (P.units_smem && T_units_large(tb)) {
+      // large unit tables are read through L1 instead when staging them
+      // would not fit or would cost resident blocks (128 registers/thread)
+      int sm_per_sm = 0, dev = ctx->device;
+      cudaDeviceGetAttribute(&sm_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
       P.units_smem = 0;
-      sm = run_smem(tb, n_specs, tpb, W, P);
+      const size_t without = run_smem(tb, n_specs, tpb, W, P);
+      const int by_regs = 65536 / (128 * tpb);
+      auto resident = [&](size_t b) { return std::min(by_regs, (int)((size_t)sm_per_sm / (b + 1024))); };
+      if ((int)sm <= ctx->max_smem && resident(sm) >= resident(without)) P.units_smem = 1;
+      else sm = without;
     }
     if ((int)sm > ctx->max_smem && P.fast_smem) {  // no room for the fast-scan tables
       P.fast_smem = 0;

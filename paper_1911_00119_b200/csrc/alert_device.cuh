@@ -973,28 +973,17 @@ __device__ __forceinline__ bool fast_max_accuracy(const DevTable& T, const float
   const bool store = W == 1 && x.has_sv;
   int u_end = lane;
   // the next unit and its bound are loaded one iteration ahead (their
-  // latency hides behind the current unit); at W > 1 the lanes stop on the
-  // tile's smallest P2 (a lane holding two keys <= lb already excludes every
-  // later unit from the tile's top 2), shared every iteration
+  // latency hides behind the current unit)
   float lb_n = lane < n_units ? lb_at(lane) : kInfF;
   int2 un_n = lane < n_units ? unit_at(lane) : make_int2(0, 0);
-  // (the tile iterates together until every lane is done: bounds only grow
-  // along the sorted units and the tile's P2 only falls, so a lane stays done)
-  for (int u = lane;; u += W) {
+  for (int u = lane; u < n_units; u += W) {
     const float lb = lb_n;
     const int2 un = un_n;
     if (u + W < n_units) {
       lb_n = lb_at(u + W);
       un_n = unit_at(u + W);
     }
-    float p2_tile = t.p2;
-    if (W > 1) {
-#pragma unroll
-      for (int o = 1; o < W; o <<= 1) p2_tile = fminf(p2_tile, tile.shfl_xor(p2_tile, o));
-    }
-    const bool done = u >= n_units || lb >= p2_tile;
-    if (W > 1 ? tile.all(done) : done) break;
-    if (done) continue;
+    if (lb >= t.p2) break;
     u_end = u + W;
     if (!((kinds >> ((un.y >> 16) ? 1 : 0)) & 1)) continue;
     const int n = un.y & 0xFFFF;
@@ -1425,7 +1414,7 @@ __device__ __forceinline__ Decision alert_decide_full(const DevTable& T, const f
 
 // Mode sets compiled into a kernel: every mode, or min-energy only (smaller
 // code and register footprint when every spec of a launch minimises energy).
-enum { MS_ALL = 0, MS_MIN_ENERGY = 1 };
+enum { MS_ALL = 0, MS_MIN_ENERGY = 1, MS_MAX_ACCURACY = 2 };
 
 // The full scan as an out-of-line call: in the min-energy kernel it runs only
 // when the fast scan cannot certify (rare), so its registers are saved around
@@ -1476,7 +1465,7 @@ __device__ __forceinline__ Decision alert_decide(const DevTable& T, const float4
 #define ALERT_OUTLINE_FULL 0
 #endif
   constexpr bool OUT = ALERT_OUTLINE_FULL && MS == MS_MIN_ENERGY;
-  if (MS == MS_MIN_ENERGY || x.spec->mode == ALERT_MODE_MIN_ENERGY) {
+  if (MS == MS_MIN_ENERGY || (MS == MS_ALL && x.spec->mode == ALERT_MODE_MIN_ENERGY)) {
     if (x.spec->has_pr)
       return alert_decide_t<ALERT_MODE_MIN_ENERGY, true, OUT>(T, sA, sB, sCol, tile, x, kinds, no_refine);
     return alert_decide_t<ALERT_MODE_MIN_ENERGY, false, OUT>(T, sA, sB, sCol, tile, x, kinds, no_refine);

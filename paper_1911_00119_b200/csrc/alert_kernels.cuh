@@ -32,6 +32,7 @@ struct RunParams {
   int c64_smem, ratio_smem, sv_smem;  // staging decisions (host computed)
   int min_energy_only;                 // every spec minimises energy: MS_MIN_ENERGY kernel
   int any_min_energy;                  // some spec minimises energy (per-tile z-threshold slots needed)
+  int max_accuracy_only;               // every spec maximises accuracy: MS_MAX_ACCURACY kernel (W = 1, 8)
   int spec_shared;                     // all specs staged once per block (few specs), not per tile
   // min-energy fast scan: per (spec, traditional DNN) z-thresholds, row
   // stride n_tdnn + 1 (last = pr_threshold bound), from zlo_kernel; null = off
@@ -726,6 +727,9 @@ inline cudaError_t launch_persistent(K kern, const RunParams& P, long long block
     if (pf == PF_BOTH) return launch_persistent(run_kernel<W, PF_BOTH, MS_ALL>, P, blocks, tpb, smem, st); \
     if (P.min_energy_only)                                                                            \
       return launch_persistent(run_kernel<W, PF_ALERT, MS_MIN_ENERGY>, P, blocks, tpb, smem, st);     \
+    if constexpr (W == 1 || W == 8)  /* the widths the library picks by default */                    \
+      if (P.max_accuracy_only)                                                                        \
+        return launch_persistent(run_kernel<W, PF_ALERT, MS_MAX_ACCURACY>, P, blocks, tpb, smem, st);   \
     return launch_persistent(run_kernel<W, PF_ALERT, MS_ALL>, P, blocks, tpb, smem, st);              \
   }                                                                                                   \
   template <>                                                                                         \
