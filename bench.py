@@ -646,7 +646,7 @@ def main():
                        "steps_per_stream": N, "candidates": C, "policy": policy, "records": args.records,
                        "goal_changes_per_stream": args.goal_changes,
                        "lanes_per_stream": lanes or (1 if C <= 256 else 8),
-                       "threads_per_block": tpb if args.tpb else "auto (64; 256 when the staged table > 40 KB)",
+                       "threads_per_block": tpb if args.tpb else "auto (64; 512 when the staged table > 40 KB)",
                        "l2": "inputs larger than L2" if flush is None else
                              "L2 flushed before every step (256 MB write, outside the step's events)",
                        "parallelism": f"items sharded (dist.shard, contiguous), {world} rank(s), {scaling} scaling"},

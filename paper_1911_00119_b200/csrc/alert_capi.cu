@@ -359,7 +359,7 @@ int alert_set_launch(AlertContext* ctx, int lanes, int tpb) {
   if (!ctx) return fail(ALERT_ERR_INVALID_ARGUMENT, "ctx is NULL");
   if (lanes != 0 && lanes != 1 && lanes != 2 && lanes != 4 && lanes != 8 && lanes != 16 && lanes != 32)
     return fail(ALERT_ERR_INVALID_ARGUMENT, "lanes_per_stream must be 0 or a power of two <= 32");
-  if (tpb != 0 && (tpb < 32 || tpb > 256 || tpb % 32))
+  if (tpb != 0 && (tpb < 32 || tpb > 512 || tpb % 32))
     return fail(ALERT_ERR_INVALID_ARGUMENT, "threads_per_block must be a multiple of 32 in [32, 256]");
   ctx->lanes = lanes;
   ctx->tpb = tpb ? tpb : 64;
@@ -1050,13 +1050,20 @@ int alert_run(AlertContext* ctx, const AlertTable* tb, const AlertFilterConfig* 
   };
   // Block size: 64 threads by default (fine-grained waves for ~10^4-10^5
   // streams); a large table (shared memory per block > 40 KB) with enough
-  // streams gets 256-thread blocks so the staged table is shared by 4x more
+  // streams gets 512-thread blocks so the staged table is shared by 8x more
   // tiles and occupancy is not capped by shared memory.
   int tpb = ctx->tpb;
   size_t smem = stage(tpb);
   if (ctx->tpb_auto && smem > 40 * 1024 && (stream_end - stream_begin) * W >= 148LL * 2 * 256) {
-    tpb = 256;
+    // one 512-thread block per SM holds the table once (two 256-thread
+    // blocks hold it twice) at the same 16 warps: room for the unit table
+    // (c4: +6%, c5: +4% measured); 256 when 512 does not fit
+    tpb = 512;
     smem = stage(tpb);
+    if ((int)smem > ctx->max_smem) {
+      tpb = 256;
+      smem = stage(tpb);
+    }
   }
   if ((int)smem > ctx->max_smem) return fail(ALERT_ERR_UNSUPPORTED, "alert_run: table exceeds shared memory");
   idle_table(*cfg, P);
@@ -1205,12 +1212,12 @@ int alert_decide(AlertContext* ctx, const AlertTable* tb, const AlertSpec* specs
   P.n = n;
   cudaError_t e;
   switch (pick_lanes(ctx, tb)) {
-    case 1: e = launch_decide<1>(P, decision, ctx->tpb, smem, s); break;
-    case 2: e = launch_decide<2>(P, decision, ctx->tpb, smem, s); break;
-    case 4: e = launch_decide<4>(P, decision, ctx->tpb, smem, s); break;
-    case 8: e = launch_decide<8>(P, decision, ctx->tpb, smem, s); break;
-    case 16: e = launch_decide<16>(P, decision, ctx->tpb, smem, s); break;
-    default: e = launch_decide<32>(P, decision, ctx->tpb, smem, s); break;
+    case 1: e = launch_decide<1>(P, decision, std::min(ctx->tpb, 256), smem, s); break;
+    case 2: e = launch_decide<2>(P, decision, std::min(ctx->tpb, 256), smem, s); break;
+    case 4: e = launch_decide<4>(P, decision, std::min(ctx->tpb, 256), smem, s); break;
+    case 8: e = launch_decide<8>(P, decision, std::min(ctx->tpb, 256), smem, s); break;
+    case 16: e = launch_decide<16>(P, decision, std::min(ctx->tpb, 256), smem, s); break;
+    default: e = launch_decide<32>(P, decision, std::min(ctx->tpb, 256), smem, s); break;
   }
   if (e != cudaSuccess) r = fail(ALERT_ERR_CUDA, std::string("decide_kernel: ") + cudaGetErrorString(e));
   cudaFreeAsync(dspecs, s);

@@ -1193,18 +1193,21 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
   int bi = -1;
   unsigned mlo = 0u, mhi = 0u;
   float acc = 0.0f;
-  for (int i = 0; i < n_seq; ++i) {
-    const float4 A = f4(aqa + 16u * i);
-    const float4 M = f4(aqm + 16u * i);
-    // stop once no later unit (nor the rest of this one) can be P1, P2 or tied with P1
-    if (M.x >= p2 && M.x > pd) break;
+  // per cell: the order-independent part (deadline penalty, Phi, energy),
+  // then the running accuracy, the key, the top 2 and the marks in order.
+  // (Two cells in flight per iteration measured 5% slower on c3: more
+  // registers, and the jumps drop the second cell.)
+  auto part = [&](const float4& A, float& pp, float& ph, float& E, float& pen) {
+    pp = HAS_PR ? fmaf(mgH, A.x, x.Tpr) : -kInfF;
+    ph = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
+    E = energy(A);
+    pen = fmaxf(fmaf(E, kPenH, elH), pp);
+  };
+  // the order-dependent part; returns the next index - 1 (i = no jump)
+  auto take = [&](int i, const float4& A, const float4& M, float pp, float ph, float E, float pen) {
     const unsigned w = __float_as_uint(M.w);
-    const float pp = HAS_PR ? fmaf(mgH, A.x, x.Tpr) : -kInfF;
     const bool skip = pp * M.y > 0.0f;  // unit start of a group the deadline bound kills
     acc = fmaf(acc, M.z, A.w);          // chain carry (0 at a unit start: restart at q_fail)
-    const float ph = phi32_x(fmaf(x.goal_f, A.x, -x.mu_f) * x.inv_sig_s);
-    const float E = energy(A);
-    const float pen = fmaxf(fmaf(E, kPenH, elH), pp);
     acc = fmaf(ph, A.z, acc);
     // surely infeasible at L0 (see fast_max_accuracy): no key; with monotone
     // stage latencies the rest of the chain is out too (host: target = next
@@ -1222,7 +1225,16 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
       mlo |= shl(1u, (unsigned)i);
       mhi |= shl(1u, (unsigned)(i - 32));
     }
-    i = nxt;
+    return nxt;
+  };
+  for (int i = 0; i < n_seq; ++i) {
+    const float4 A = f4(aqa + 16u * i);
+    const float4 M = f4(aqm + 16u * i);
+    // stop once no later unit (nor the rest of this one) can be P1, P2 or tied with P1
+    if (M.x >= p2 && M.x > pd) break;
+    float pp, ph, E, pen;
+    part(A, pp, ph, E, pen);
+    i = take(i, A, M, pp, ph, E, pen);
   }
   if (!(p1 < 2.0f) || bi < 0) return false;  // P1 must be a possible cell (no penalty)
   const int c1 = (int)((meta_w(bi) >> 8) & 0xFFu);

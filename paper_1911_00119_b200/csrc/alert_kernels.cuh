@@ -206,7 +206,7 @@ __device__ __forceinline__ void fill_ratios(const DevTable& T, const Tile& tile,
 #define ALERT_ALL_REGS 128
 #endif
 template <int W, int PF, int MS>
-__global__ void __launch_bounds__(256) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_MINE_REGS : ALERT_ALL_REGS)
+__global__ void __launch_bounds__(512) __maxnreg__(MS == MS_MIN_ENERGY ? ALERT_MINE_REGS : ALERT_ALL_REGS)
     run_kernel(const RunParams P) {
   extern __shared__ float4 smem[];
   const DevTable& T = P.T;
