@@ -454,11 +454,16 @@ def main():
 
     import torch
 
+    # one process per GPU; more ranks than GPUs (a code-path check on a
+    # one-GPU box) share the devices round-robin and need ALERT_DIST_BACKEND=gloo
+    # (NCCL refuses two ranks on one device)
+    shared = world > torch.cuda.device_count()
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
 
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group(os.environ.get("ALERT_DIST_BACKEND", "nccl"), init_method="env://")
     else:
         torch.cuda.set_device(local)
     import paper_1911_00119_b200 as A
@@ -649,7 +654,8 @@ def main():
                        "threads_per_block": tpb if args.tpb else "auto (64; 512 when the staged table > 40 KB)",
                        "l2": "inputs larger than L2" if flush is None else
                              "L2 flushed before every step (256 MB write, outside the step's events)",
-                       "parallelism": f"items sharded (dist.shard, contiguous), {world} rank(s), {scaling} scaling"},
+                       "parallelism": f"items sharded (dist.shard, contiguous), {world} rank(s), {scaling} scaling"
+                                      + (" [ranks share GPUs: a code-path check, not a scaling number]" if shared else "")},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
             "clocks": clocks, "quality": quality,
         }

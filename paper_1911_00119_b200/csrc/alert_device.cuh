@@ -1260,7 +1260,9 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
     while (marks) {
       const int i = __ffsll((long long)marks) - 1;
       marks &= marks - 1;
-      const unsigned mw = meta_w(i);
+      const float4 Mi = f4(aqm + 16u * i);
+      if (Mi.x > cut) continue;  // every key of the cell's unit is >= its bound: outside the final cut
+      const unsigned mw = __float_as_uint(Mi.w);
       const int k = (int)(mw & 7u), c = (int)((mw >> 8) & 0xFFu);
       float a = 0.f, tail = 0.f, r = 0.f;
       bool bad = false;

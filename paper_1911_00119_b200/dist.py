@@ -29,12 +29,15 @@ def reduce_aggregates(local, group=None):
 
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return local.clone()
-    parts = [torch.empty_like(local) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(parts, local.contiguous(), group=group)
+    src = local.contiguous()
+    if dist.get_backend(group) == "gloo" and src.is_cuda:  # gloo gathers host tensors
+        src = src.cpu()
+    parts = [torch.empty_like(src) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, src, group=group)
     total = parts[0].clone()
     for p in parts[1:]:
         total += p
-    return total
+    return total.to(local.device)
 
 
 def max_over_ranks(value: float, device=None, group=None) -> float:
@@ -44,7 +47,8 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
 
     if not dist.is_available() or not dist.is_initialized():
         return value
-    t = torch.tensor([value], dtype=torch.float64, device=device)
+    gloo = dist.get_backend(group) == "gloo"
+    t = torch.tensor([value], dtype=torch.float64, device=None if gloo else device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
 
@@ -56,6 +60,7 @@ def sum_over_ranks(value: float, device=None, group=None) -> float:
 
     if not dist.is_available() or not dist.is_initialized():
         return value
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    gloo = dist.get_backend(group) == "gloo"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=None if gloo else device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return float(t.item())
