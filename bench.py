@@ -229,7 +229,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def mark(self, begin: bool):
+        """Host times bracketing the timed region (samples outside are not reported)."""
+        if begin:
+            self.t0 = time.monotonic()
+        else:
+            self.t1 = time.monotonic()
 
     def __exit__(self, *exc):
         if self.proc:
@@ -241,7 +248,9 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        inside = [ln for t, ln in self.lines if t0 is None or t1 is None or t0 <= t <= t1 + 0.06]
+        for ln in inside or [ln for _, ln in self.lines[-3:]]:
             try:
                 a, b, c = [x.strip() for x in ln.split(",")]
                 sm.append(float(a))
@@ -522,6 +531,10 @@ def main():
             b.record(stream)
             kev.append((a, b))
 
+    # the clock sampler (an nvidia-smi process) starts before the warm-up, so
+    # its start-up never overlaps the timed region; only samples taken during
+    # the timed region are reported
+    clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         step(False)
     torch.cuda.synchronize(dev)
@@ -530,12 +543,14 @@ def main():
         dist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            step(True)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
+    clk.mark(True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk.mark(False)
+    clk.__exit__(None, None, None)
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)

@@ -605,6 +605,21 @@ struct Top2 {
     p2 = fmin3(fmaxf(p1, lo), p2, hi);
     p1 = fminf(p1, lo);
   }
+  // eight keys: their top 2 by a tournament (independent of the running
+  // pair), then one merge — the loop-carried chain is 3 operations, not 10
+  __device__ __forceinline__ void push8(const float (&k)[8]) {
+    float lo[4], hi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      lo[j] = fminf(k[2 * j], k[2 * j + 1]);
+      hi[j] = fmaxf(k[2 * j], k[2 * j + 1]);
+    }
+    const float a1 = fminf(lo[0], lo[1]), a2 = fmin3(fmaxf(lo[0], lo[1]), hi[0], hi[1]);
+    const float b1 = fminf(lo[2], lo[3]), b2 = fmin3(fmaxf(lo[2], lo[3]), hi[2], hi[3]);
+    const float m1 = fminf(a1, b1), m2 = fmin3(fmaxf(a1, b1), a2, b2);
+    p2 = fmin3(fmaxf(p1, m1), p2, m2);
+    p1 = fminf(p1, m1);
+  }
   template <class Tile>
   __device__ __forceinline__ void merge(const Tile& tile) {
 #pragma unroll
@@ -710,8 +725,7 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
           const float kk = pack_key(A.y * fmax3(x.mu_e, fmaf(x.phig, A.x, x.ompmu), fmaf(mgH, A.x, Td)), u);
           k[u] = p0 + u * W < P ? kk : kInfF;
         }
-#pragma unroll
-        for (int u = 0; u < 8; u += 2) t.push2(k[u], k[u + 1]);
+        t.push8(k);
         if (t.p1 != s1) t.blk = dn * P + p0;
       }
     }
@@ -730,8 +744,7 @@ __device__ __forceinline__ bool fast_min_energy(const DevTable& T, const float4*
       float k[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) k[u] = key_of(sF[c + u * W], c + u * W);
-#pragma unroll
-      for (int u = 0; u < 8; u += 2) t.push2(k[u], k[u + 1]);
+      t.push8(k);
       if (t.p1 != s1) t.blk = c;
     }
     // remainder (< 8 cells) in quarter-chunks: positions 0-3 then 4-7 of the
