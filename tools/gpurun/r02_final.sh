@@ -4,10 +4,10 @@
 # DRAM traffic at the bench shapes, compute-sanitizer.
 mkdir -p gpurun_out
 bash tools/gpurun/tests.sh
-timeout 900 python bench.py > gpurun_out/f_c2.json 2> gpurun_out/f_c2.err; tail -1 gpurun_out/f_c2.json | cut -c1-200
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/f_c2.json 2> gpurun_out/f_c2.err; tail -1 gpurun_out/f_c2.json | cut -c1-200
 timeout 900 python bench.py --config c3 > gpurun_out/f_c3.json 2> gpurun_out/f_c3.err; tail -1 gpurun_out/f_c3.json | cut -c1-200
-timeout 1500 python bench.py --config c4 --steps 1 > gpurun_out/f_c4.json 2> gpurun_out/f_c4.err; tail -1 gpurun_out/f_c4.json | cut -c1-200
-timeout 1800 python bench.py --config c5 --steps 1 > gpurun_out/f_c5.json 2> gpurun_out/f_c5.err; tail -1 gpurun_out/f_c5.json | cut -c1-200
+timeout 1500 python bench.py --config c4 --steps 1 --warmup 3 > gpurun_out/f_c4.json 2> gpurun_out/f_c4.err; tail -1 gpurun_out/f_c4.json | cut -c1-200
+timeout 1800 python bench.py --config c5 --steps 1 --warmup 3 > gpurun_out/f_c5.json 2> gpurun_out/f_c5.err; tail -1 gpurun_out/f_c5.json | cut -c1-200
 timeout 900 python bench.py --config c1 > gpurun_out/f_c1.json 2> gpurun_out/f_c1.err; tail -1 gpurun_out/f_c1.json | cut -c1-200
 timeout 900 python bench.py --config c2 --goal-changes 4 --steps 3 > gpurun_out/f_c2g.json 2> gpurun_out/f_c2g.err; tail -1 gpurun_out/f_c2g.json | cut -c1-200
 timeout 600 python bench.py --impl reference > gpurun_out/f_ref.json 2> gpurun_out/f_ref.err; tail -1 gpurun_out/f_ref.json | cut -c1-200
@@ -16,3 +16,4 @@ bash tools/gpurun/prof_cfg.sh c2f --trace-steps 1000
 bash tools/gpurun/prof_cfg.sh c3f --config c3 --total-streams 1048576 --trace-steps 100
 bash tools/gpurun/prof_skip.sh c5maxf 1 --config c5 --total-streams 65536 --trace-steps 100
 bash tools/gpurun/prof_skip.sh c4maxf 1 --config c4 --total-streams 65536 --trace-steps 100
+bash tools/gpurun/sanitize.sh
