@@ -210,13 +210,52 @@ def n_candidates(space) -> int:
 # clocks sampled during the timed region
 
 class ClockSampler:
+    """SM clock / max clock / event reasons during the timed region: NVML
+    polled every 2 ms from a thread (in-process; short timed regions such as
+    c1's ~15 ms still get samples), else an ``nvidia-smi -lms 50`` process.
+    Samples are lines "sm, max, 0xreasons" with their host time."""
+
     def __init__(self, device: int):
         self.device = device
         self.proc = None
         self.lines = []
+        self.source = None
+        self._stop = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+        uuid = uuid if uuid.startswith("GPU-") else "GPU-" + uuid
+        try:
+            return pynvml, pynvml.nvmlDeviceGetHandleByUUID(uuid)
+        except pynvml.NVMLError:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.device)
+
+    def _poll_nvml(self, nv, h):
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.lines.append((time.monotonic(), f"{sm}, {mx}, {rs:#x}"))
+            except nv.NVMLError:
+                return
+            time.sleep(0.002)
 
     def __enter__(self):
         try:
+            nv, h = self._nvml_handle()
+            self.source = "nvml (2 ms)"
+            self.t = threading.Thread(target=self._poll_nvml, args=(nv, h), daemon=True)
+            self.t.start()
+            return self
+        except Exception:  # no NVML binding / device: the nvidia-smi process below
+            pass
+        try:
+            self.source = "nvidia-smi (50 ms)"
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
@@ -239,6 +278,7 @@ class ClockSampler:
             self.t1 = time.monotonic()
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -262,8 +302,9 @@ class ClockSampler:
             except ValueError:
                 continue
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": self.source}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": self.source}
 
 
 # --------------------------------------------------------------------------

@@ -16,4 +16,4 @@ bash tools/gpurun/prof_cfg.sh c2f --trace-steps 1000
 bash tools/gpurun/prof_cfg.sh c3f --config c3 --total-streams 1048576 --trace-steps 100
 bash tools/gpurun/prof_skip.sh c5maxf 1 --config c5 --total-streams 65536 --trace-steps 100
 bash tools/gpurun/prof_skip.sh c4maxf 1 --config c4 --total-streams 65536 --trace-steps 100
-bash tools/gpurun/sanitize.sh
+# compute-sanitizer is closed on the GPU pool since the round-2 logs in profiles/r02_sanitizer_*.log
