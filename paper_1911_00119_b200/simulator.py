@@ -173,6 +173,36 @@ def _run_batch(eng, torch, space, specs, envs, policy, kalman, idle_cfg, group_s
     )
 
 
+def chunk_sizes(n_steps: int, chunk: int, tail: bool = True, growth: float = 1.4) -> list[int]:
+    """Step-chunk lengths for HostStreamer.  The head ramps up geometrically
+    from chunk / 8 (each copy short enough to finish while the previous
+    chunk computes, so the kernel never waits after the first, short copy),
+    then full chunks.  With ``tail`` the last chunk is short too (copy-bound
+    runs: little kernel time after the last copy); without it the last chunk
+    stays long enough to hide the aggregate D2H behind its stream-range
+    launches."""
+    if n_steps <= 0:
+        raise ValueError("n_steps must be positive")
+    chunk = max(1, min(chunk, n_steps))
+    edge = max(1, chunk // 8)
+    if n_steps <= chunk:
+        return [n_steps]
+    sizes, rem, z = [], n_steps, edge
+    while z < chunk and rem > z + (edge if tail else 0):
+        sizes.append(z)
+        rem -= z
+        z = min(chunk, max(z + 1, int(z * growth)))
+    if not tail:  # a partial chunk right after the ramp, full chunks to the end
+        if rem % chunk:
+            sizes.append(rem % chunk)
+        return sizes + [chunk] * (rem // chunk)
+    while rem > chunk + edge:
+        sizes.append(chunk)
+        rem -= chunk
+    sizes += [rem - edge, edge] if rem > edge else [rem]
+    return sizes
+
+
 class HostStreamer:
     """run_batch for traces that live in (pinned) HOST memory.
 
@@ -183,11 +213,20 @@ class HostStreamer:
     The scenario map (stream_spec, and stream_row when scenarios share trace
     rows) is copied from pinned host memory at the start of every pass.
     This is the end-to-end path: inputs from host, per-stream summaries back.
+
+    Pipeline edges: the first step chunk is short (chunk / 8) so the first
+    copy is short; with one D2H part the last chunk is short too (little
+    kernel time after the last copy); with many streams (``d2h_parts`` > 1, default one part per
+    131,072 streams, at most 8) the last chunk runs as stream-range launches
+    and each range's aggregate rows go device->host on the copy stream while
+    the next range computes.  The returned tensor is ready once the caller's
+    current stream has synchronised (it waits on the copy stream).
     """
 
     def __init__(self, space, specs, packed: PackedEnvs, policy: str = "alert", *, kalman=None,
                  idle_cfg=None, group_sizes=None, stream_spec=None, stream_row=None, chunk_steps: int = 1000,
-                 engine: Engine | None = None, device: int = 0):
+                 engine: Engine | None = None, device: int = 0, d2h_parts: int | None = None,
+                 schedule: Sequence[int] | None = None):
         torch = __import__("torch")
         self.torch = torch
         self.eng = eng = engine or get_engine(device)
@@ -202,6 +241,13 @@ class HostStreamer:
         self.n_steps, n_rows = packed.slowdown.shape
         self.n_streams = n_rows if stream_row is None else len(stream_row)
         self.chunk = min(chunk_steps, self.n_steps)
+        self.d2h_parts = max(1, min(8, self.n_streams // 131072)) if d2h_parts is None else int(d2h_parts)
+        if not 1 <= self.d2h_parts <= self.n_streams:
+            raise ValueError(f"d2h_parts must be in 1..{self.n_streams}")
+        self.sizes = chunk_sizes(self.n_steps, self.chunk, tail=self.d2h_parts == 1) if schedule is None \
+            else [int(z) for z in schedule]
+        if sum(self.sizes) != self.n_steps or min(self.sizes) < 1 or max(self.sizes) > self.chunk:
+            raise ValueError(f"schedule must split {self.n_steps} steps into chunks of 1..{self.chunk}")
         d = eng.tdev
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
         # pinned host copies of the inputs (outside any timed region)
@@ -251,34 +297,49 @@ class HostStreamer:
         stream_row = self.map_dev[1] if len(self.map_dev) > 1 else None
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         consumed = [torch.cuda.Event(), torch.cuda.Event()]
-        starts = list(range(0, self.n_steps, self.chunk))
+        starts = np.concatenate([[0], np.cumsum(self.sizes)]).tolist()
+        n_chunks = len(self.sizes)
 
         def issue_copy(i):
             b = i % 2
-            s0 = starts[i]
-            s1 = min(self.n_steps, s0 + self.chunk)
+            s0, s1 = starts[i], starts[i + 1]
             with torch.cuda.stream(self.copy_stream):
                 if i >= 2:
                     self.copy_stream.wait_event(consumed[b])
                 self.bufs[b][: s1 - s0].copy_(self.host[s0:s1], non_blocking=True)
                 copied[b].record(self.copy_stream)
 
+        def launch(tr, s0, s1, b0, b1):  # the goal-mode runs intersected with streams [b0, b1)
+            for k, (lb, le, sp) in enumerate(self.runs):
+                lo, hi = max(lb, b0), min(le, b1)
+                if lo < hi:
+                    eng.run(self.table, sp, tr, state, policy=self.policy, kalman=self.kalman,
+                            idle_cfg=self.idle_cfg, stream_spec=self.map_dev[0][k], outputs=out, stream_begin=lo,
+                            stream_end=hi, step_begin=s0, step_end=s1, flags=abi.FLAG_FRESH if s0 == 0 else 0)
+
         issue_copy(0)
-        for i, s0 in enumerate(starts):
-            s1 = min(self.n_steps, s0 + self.chunk)
-            if i + 1 < len(starts):
+        for i in range(n_chunks):
+            s0, s1 = starts[i], starts[i + 1]
+            if i + 1 < n_chunks:
                 issue_copy(i + 1)
             b = i % 2
             comp.wait_event(copied[b])
             tr = DeviceTrace(self.bufs[b][: s1 - s0], *self.seg, stream_row=stream_row, step_offset=s0)
             if self.goals is not None:
                 tr.goal_n, tr.goal_end, tr.goal_spec = self.goals
-            for k, (lb, le, sp) in enumerate(self.runs):
-                eng.run(self.table, sp, tr, state, policy=self.policy, kalman=self.kalman,
-                        idle_cfg=self.idle_cfg, stream_spec=self.map_dev[0][k], outputs=out, stream_begin=lb,
-                        stream_end=le, step_begin=s0, step_end=s1, flags=abi.FLAG_FRESH if s0 == 0 else 0)
+            if i + 1 < n_chunks:
+                launch(tr, s0, s1, 0, self.n_streams)
+            else:  # last chunk: stream ranges, each range's final aggregates D2H behind the next range
+                cuts = [self.n_streams * p // self.d2h_parts for p in range(self.d2h_parts + 1)]
+                for p in range(self.d2h_parts):
+                    launch(tr, s0, s1, cuts[p], cuts[p + 1])
+                    done = torch.cuda.Event()
+                    done.record(comp)
+                    with torch.cuda.stream(self.copy_stream):
+                        self.copy_stream.wait_event(done)
+                        self.agg_host[cuts[p]:cuts[p + 1]].copy_(agg[cuts[p]:cuts[p + 1]], non_blocking=True)
             consumed[b].record(comp)
-        self.agg_host.copy_(agg, non_blocking=True)
+        comp.wait_stream(self.copy_stream)  # the caller's stream covers the D2H
         return self.agg_host
 
 

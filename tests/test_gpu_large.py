@@ -99,6 +99,27 @@ def test_host_streamer_matches_device_resident(c2):
     agg = hs.run()
     torch.cuda.synchronize()
     np.testing.assert_array_equal(agg.numpy(), dev.agg)
+    # last chunk as stream ranges with the aggregate D2H overlapped (uneven cuts), twice in a row
+    hs = HostStreamer(space, A.pack_specs(specs), packed, "alert", chunk_steps=2000, d2h_parts=3)
+    for _ in range(2):
+        agg = hs.run()
+        torch.cuda.current_stream().synchronize()
+        np.testing.assert_array_equal(agg.numpy(), dev.agg)
+
+
+def test_host_streamer_stream_ranges_grid():
+    """Shared trace rows + two goal modes + a last chunk split into stream
+    ranges that cut through the mode runs: equal to the device-resident run."""
+    from paper_1911_00119_b200.simulator import HostStreamer
+
+    space, specs, packed, ss, sr = _grid(n_traces=16, steps=300)
+    dev = A.run_batch(space, A.pack_specs(specs), packed, "alert", stream_spec=ss, stream_row=sr)
+    for parts in (1, 5):
+        hs = HostStreamer(space, A.pack_specs(specs), packed, "alert", stream_spec=ss, stream_row=sr,
+                          chunk_steps=64, d2h_parts=parts)
+        agg = hs.run()
+        torch.cuda.current_stream().synchronize()
+        np.testing.assert_array_equal(agg.numpy(), dev.agg)
 
 
 def _grid(n_traces=64, steps=300):

@@ -100,3 +100,22 @@ def test_baseline_dnn_choice_matches_reference_rules():
     assert baseline_dnns(only_any) == (-1, 0)
     with pytest.raises(ValueError, match="TRADITIONAL"):
         A.make_policy("sys-only").begin(only_any, None, None)
+
+
+def test_host_streamer_chunk_schedule():
+    """HostStreamer's step chunks: cover the trace exactly, never exceed the
+    buffer, short head and tail around full chunks."""
+    from paper_1911_00119_b200.simulator import chunk_sizes
+
+    for n in (1, 2, 9, 17, 300, 1000, 10000, 12345):
+        for c in (1, 3, 8, 100, 777, 1000, 20000):
+            z = chunk_sizes(n, c)
+            assert sum(z) == n and min(z) > 0 and max(z) <= min(c, n)
+    z = chunk_sizes(10000, 1000)
+    assert z[:3] == [125, 175, 244] and z[-1] == 125 and z.count(1000) >= 6
+    assert all(b <= 1.4 * a + 1 for a, b in zip(z, z[1:]) if b < 1000)  # geometric head
+    assert chunk_sizes(1000, 100)[0] == 12 and chunk_sizes(1000, 100)[-1] == 12
+    assert chunk_sizes(300, 777) == [300]
+    for n in (9, 1000, 12345):
+        z = chunk_sizes(n, 100, tail=False)
+        assert sum(z) == n and max(z) <= 100 and (n <= 100 or (z[0] == 12 and z[-1] == 100))  # long last chunk
