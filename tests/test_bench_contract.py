@@ -98,3 +98,19 @@ def test_goal_change_workload():
     p = wl["packed"]
     assert (p.goal_n == 3).all()
     np.testing.assert_array_equal(p.goal_end[0], [30, 60, 90])
+
+
+def test_clock_summary_keeps_timed_region_samples_and_reasons():
+    """Clock samples ("sm, max, 0xreasons" lines, NVML or nvidia-smi) are
+    reported only from inside the timed region; idle is not a reason,
+    thermal slowdown is."""
+    cs = _bench().ClockSampler(0)
+    cs.source = "test"
+    cs.t0, cs.t1 = 10.0, 11.0
+    cs.lines = [(9.0, "1000, 1965, 0x1"), (10.2, "1965, 1965, 0x0"), (10.4, "1965, 1965, 0x0"),
+                (10.6, "1950, 1965, 0x20"), (12.0, "500, 1965, 0x8")]
+    s = cs.summary()
+    assert s["samples"] == 3 and s["sm_mhz"] == 1965.0 and s["sm_max_mhz"] == 1965.0
+    assert s["reasons"] == ["sw_thermal_slowdown"] and s["source"] == "test"
+    cs.lines = []
+    assert cs.summary()["samples"] == 0
