@@ -93,3 +93,41 @@ def test_table_past_the_limit_is_rejected():
     space = A.generate_space(A.ProfileKnobs(n_dnns=93, n_powers=65))
     with pytest.raises(ValueError, match="candidates"):
         A.run_batch(space, _specs(space)[:1], preset_batch(1, lengths=(4, 4, 4), processes=1), "alert")
+
+
+def test_degenerate_and_ragged_shapes():
+    """One stream x one input; one-input phases; stream counts that do not
+    fill a warp (W = 1) or a tile group (W = 8); an empty stream range
+    through the C ABI is a no-op (no launch, outputs untouched)."""
+    space = A.preset_space()
+    ref = A.reference_latency(space)
+    spec = A.ConstraintSpec(mode=A.Mode.MINIMIZE_ENERGY, t_goal=0.14, q_goal=0.68, overhead_budget=0.01 * ref)
+    # one stream, one input
+    env1 = A.realize(A.Trace(seed=7, phases=(A.EnvironmentPhase(1, A.Constant(1.0), 4.0, 0.05),)))
+    rec, agg, _ = oracle.run(space, spec, env1, "alert")
+    res = A.run_batch(space, [spec], [env1], "alert", records="f64")
+    assert res.decoded()["cand"][0, 0] == rec["cand"][0]
+    np.testing.assert_allclose(res.agg[0, :abi.AGG_LEVEL0], agg[:abi.AGG_LEVEL0], rtol=RTOL_F64)
+    # one-input phases (a segment change at every step), 33 streams at W = 1, 3 streams at W = 8
+    phases = tuple(A.EnvironmentPhase(1, A.Gaussian(1.0 + 0.2 * k, 0.1), 3.0 + k, 0.05) for k in range(3))
+    for n, lanes in ((33, 1), (3, 8)):
+        envs = [A.realize(A.Trace(seed=100 + k, phases=phases * 2)) for k in range(n)]
+        recs = [oracle.run(space, spec, e, "alert") for e in envs]
+        res = A.run_batch(space, [spec], envs, "alert", records="f64", trace_dtype=np.float64,
+                          lanes_per_stream=lanes)
+        for k, (rec, agg, _) in enumerate(recs):
+            np.testing.assert_array_equal(res.decoded()["cand"][:, k], rec["cand"])
+            np.testing.assert_allclose(res.agg[k, :abi.AGG_LEVEL0], agg[:abi.AGG_LEVEL0], rtol=RTOL_F64)
+    # empty ranges: nothing launched, outputs untouched
+    eng = A.get_engine(0)
+    table = eng.table(space)
+    packed = A.pack_envs([env1, env1], dtype=np.float64)
+    trace = eng.upload_trace(packed)
+    state = eng.new_state(table, 2)
+    from paper_1911_00119_b200.engine import outputs_struct
+    agg_t = torch.full((2, abi.AGG_FIELDS), 7.0, dtype=torch.float64, device=eng.tdev)
+    before = eng.launch_count()
+    eng.run(table, A.pack_specs([spec]), trace, state, policy=abi.POLICY_ALERT, outputs=outputs_struct(None, agg=agg_t),
+            stream_begin=1, stream_end=1)
+    torch.cuda.synchronize()
+    assert eng.launch_count() == before and bool((agg_t == 7.0).all())
