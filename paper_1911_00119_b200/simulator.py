@@ -218,9 +218,12 @@ class HostStreamer:
     copy is short; with one D2H part the last chunk is short too (little
     kernel time after the last copy); with many streams (``d2h_parts`` > 1, default one part per
     131,072 streams, at most 8) the last chunk runs as stream-range launches
-    and each range's aggregate rows go device->host on the copy stream while
-    the next range computes.  The returned tensor is ready once the caller's
-    current stream has synchronised (it waits on the copy stream).
+    and each range's aggregate rows go device->host on a second copy stream while
+    the next range computes.  Back-to-back passes overlap: a pass's first
+    copies wait only for the previous pass's last use of each trace buffer,
+    so they run under its last chunks.  The returned tensor is ready once
+    the caller's current stream has synchronised (it waits on the copy
+    stream); a later pass rewrites it.
     """
 
     def __init__(self, space, specs, packed: PackedEnvs, policy: str = "alert", *, kalman=None,
@@ -273,6 +276,10 @@ class HostStreamer:
             self.map_dev.append(torch.empty_like(self.map_host[1], device=d))
         self.bufs = [torch.empty((self.chunk, n_rows), dtype=self.host.dtype, device=d) for _ in range(2)]
         self.copy_stream = torch.cuda.Stream(d)
+        # last use of each trace buffer by the previous pass: the next pass's first copies wait only for
+        # these, so they run under the previous pass's last chunks (back-to-back passes keep PCIe busy)
+        self._released = [None, None]
+        self.d2h_stream = torch.cuda.Stream(d)  # aggregate rows back, beside the H2D copies
         self.agg_host = torch.empty((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64).pin_memory()
 
     @property
@@ -288,7 +295,8 @@ class HostStreamer:
         """One end-to-end pass; returns the pinned host aggregate tensor."""
         torch, eng = self.torch, self.eng
         comp = torch.cuda.current_stream(eng.tdev)
-        self.copy_stream.wait_stream(comp)  # copies are ordered after the caller's prior work
+        if self._released[0] is None:  # first pass: copies ordered after the caller's prior work
+            self.copy_stream.wait_stream(comp)
         for h, dv in zip(self.map_host, self.map_dev):
             dv.copy_(h, non_blocking=True)
         state = eng.new_state(self.table, self.n_streams, self.kalman, self.idle_cfg, init=False)
@@ -306,6 +314,8 @@ class HostStreamer:
             with torch.cuda.stream(self.copy_stream):
                 if i >= 2:
                     self.copy_stream.wait_event(consumed[b])
+                elif self._released[b] is not None:
+                    self.copy_stream.wait_event(self._released[b])
                 self.bufs[b][: s1 - s0].copy_(self.host[s0:s1], non_blocking=True)
                 copied[b].record(self.copy_stream)
 
@@ -335,11 +345,12 @@ class HostStreamer:
                     launch(tr, s0, s1, cuts[p], cuts[p + 1])
                     done = torch.cuda.Event()
                     done.record(comp)
-                    with torch.cuda.stream(self.copy_stream):
-                        self.copy_stream.wait_event(done)
+                    with torch.cuda.stream(self.d2h_stream):
+                        self.d2h_stream.wait_event(done)
                         self.agg_host[cuts[p]:cuts[p + 1]].copy_(agg[cuts[p]:cuts[p + 1]], non_blocking=True)
             consumed[b].record(comp)
-        comp.wait_stream(self.copy_stream)  # the caller's stream covers the D2H
+        self._released = consumed
+        comp.wait_stream(self.d2h_stream)  # the caller's stream covers the D2H
         return self.agg_host
 
 
