@@ -206,9 +206,9 @@ def chunk_sizes(n_steps: int, chunk: int, tail: bool = True, growth: float = 1.4
 class HostStreamer:
     """run_batch for traces that live in (pinned) HOST memory.
 
-    The time-major slow-down array is cut into step chunks; chunk i+1 is
+    The time-major slow-down array is cut into step chunks; later chunks are
     copied host->device on a copy stream while the kernel runs chunk i on the
-    compute stream (double buffer, CUDA events), with the filter state and
+    compute stream (``n_buffers`` device buffers in a ring, CUDA events), with the filter state and
     aggregates carried on the device between chunks (alert_run step ranges).
     The scenario map (stream_spec, and stream_row when scenarios share trace
     rows) is copied from pinned host memory at the start of every pass.
@@ -229,7 +229,7 @@ class HostStreamer:
     def __init__(self, space, specs, packed: PackedEnvs, policy: str = "alert", *, kalman=None,
                  idle_cfg=None, group_sizes=None, stream_spec=None, stream_row=None, chunk_steps: int = 1000,
                  engine: Engine | None = None, device: int = 0, d2h_parts: int | None = None,
-                 schedule: Sequence[int] | None = None):
+                 schedule: Sequence[int] | None = None, n_buffers: int = 3):
         torch = __import__("torch")
         self.torch = torch
         self.eng = eng = engine or get_engine(device)
@@ -274,11 +274,13 @@ class HostStreamer:
         if stream_row is not None:
             self.map_host.append(pin(np.asarray(stream_row, np.int32)))
             self.map_dev.append(torch.empty_like(self.map_host[1], device=d))
-        self.bufs = [torch.empty((self.chunk, n_rows), dtype=self.host.dtype, device=d) for _ in range(2)]
+        if n_buffers < 2:
+            raise ValueError("n_buffers must be >= 2")
+        self.bufs = [torch.empty((self.chunk, n_rows), dtype=self.host.dtype, device=d) for _ in range(n_buffers)]
         self.copy_stream = torch.cuda.Stream(d)
         # last use of each trace buffer by the previous pass: the next pass's first copies wait only for
         # these, so they run under the previous pass's last chunks (back-to-back passes keep PCIe busy)
-        self._released = [None, None]
+        self._released = [None] * n_buffers
         self.d2h_stream = torch.cuda.Stream(d)  # aggregate rows back, beside the H2D copies
         self.agg_host = torch.empty((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64).pin_memory()
 
@@ -303,16 +305,17 @@ class HostStreamer:
         agg = torch.empty((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64, device=eng.tdev)
         out = outputs_struct(None, agg=agg)
         stream_row = self.map_dev[1] if len(self.map_dev) > 1 else None
-        copied = [torch.cuda.Event(), torch.cuda.Event()]
-        consumed = [torch.cuda.Event(), torch.cuda.Event()]
+        nb = len(self.bufs)
+        copied = [torch.cuda.Event() for _ in range(nb)]
+        consumed = [torch.cuda.Event() for _ in range(nb)]
         starts = np.concatenate([[0], np.cumsum(self.sizes)]).tolist()
         n_chunks = len(self.sizes)
 
         def issue_copy(i):
-            b = i % 2
+            b = i % nb
             s0, s1 = starts[i], starts[i + 1]
             with torch.cuda.stream(self.copy_stream):
-                if i >= 2:
+                if i >= nb:
                     self.copy_stream.wait_event(consumed[b])
                 elif self._released[b] is not None:
                     self.copy_stream.wait_event(self._released[b])
@@ -327,12 +330,13 @@ class HostStreamer:
                             idle_cfg=self.idle_cfg, stream_spec=self.map_dev[0][k], outputs=out, stream_begin=lo,
                             stream_end=hi, step_begin=s0, step_end=s1, flags=abi.FLAG_FRESH if s0 == 0 else 0)
 
-        issue_copy(0)
+        for i in range(min(nb - 1, n_chunks)):
+            issue_copy(i)
         for i in range(n_chunks):
             s0, s1 = starts[i], starts[i + 1]
-            if i + 1 < n_chunks:
-                issue_copy(i + 1)
-            b = i % 2
+            if i + nb - 1 < n_chunks:
+                issue_copy(i + nb - 1)
+            b = i % nb
             comp.wait_event(copied[b])
             tr = DeviceTrace(self.bufs[b][: s1 - s0], *self.seg, stream_row=stream_row, step_offset=s0)
             if self.goals is not None:

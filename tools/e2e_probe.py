@@ -18,32 +18,25 @@ n_steps = 1000 if cfg == "c3" else 10000
 wl = bench.build_workload(cfg, n_steps, 0, total, total)
 
 
-def timed(hs, reps=3):
+def timed(hs, reps=5):
+    """ms per pass over `reps` back-to-back passes (as bench.py's e2e loop)."""
     hs.run()
     torch.cuda.synchronize()
-    out = []
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
     for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
         hs.run()
-        b.record()
-        torch.cuda.synchronize()
-        out.append(a.elapsed_time(b))
-    return round(min(out), 2)
+    b.record()
+    torch.cuda.synchronize()
+    return round(a.elapsed_time(b) / reps, 2)
 
 
 res = {}
-variants = []  # (tag, chunk, sizes, parts)
-for chunk in (n_steps // 10, n_steps // 5):
-    variants.append((f"chunk{chunk}_plain_p1", chunk, [chunk] * (n_steps // chunk), 1))
-    for parts in (1, 8):
-        for tail in (True, False):
-            variants.append((f"chunk{chunk}_head{'_tail' if tail else ''}_p{parts}", chunk,
-                             chunk_sizes(n_steps, chunk, tail=tail), parts))
-for tag, chunk, sizes, parts in variants:
+chunk = n_steps // 10
+for nb in (3, 2, 4, 2, 3):
     hs = HostStreamer(wl["space"], wl["specs"], wl["packed"], "alert", stream_spec=wl["stream_spec"],
-                      stream_row=wl["stream_row"], chunk_steps=chunk, d2h_parts=parts, schedule=sizes)
-    res[tag] = timed(hs)
+                      stream_row=wl["stream_row"], chunk_steps=chunk, n_buffers=nb)
+    res[f"buffers{nb}_{len(res)}"] = timed(hs)
     del hs
     torch.cuda.empty_cache()
 print(json.dumps({"config": cfg, "streams": total, "steps": n_steps, "ms_per_pass": res}))
