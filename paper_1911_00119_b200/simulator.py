@@ -206,24 +206,25 @@ def chunk_sizes(n_steps: int, chunk: int, tail: bool = True, growth: float = 1.4
 class HostStreamer:
     """run_batch for traces that live in (pinned) HOST memory.
 
-    The time-major slow-down array is cut into step chunks; later chunks are
-    copied host->device on a copy stream while the kernel runs chunk i on the
-    compute stream (``n_buffers`` device buffers in a ring, CUDA events), with the filter state and
-    aggregates carried on the device between chunks (alert_run step ranges).
-    The scenario map (stream_spec, and stream_row when scenarios share trace
-    rows) is copied from pinned host memory at the start of every pass.
-    This is the end-to-end path: inputs from host, per-stream summaries back.
+    The time-major slow-down array is cut into step chunks copied
+    host->device on a copy stream into a ring of ``n_buffers`` device
+    buffers while the kernel runs earlier chunks on the compute stream (CUDA
+    events order them); the filter state and aggregates stay on the device
+    between chunks (alert_run step ranges).  The scenario map (stream_spec,
+    and stream_row when scenarios share trace rows) is copied from pinned
+    host memory at the start of every pass.  This is the end-to-end path:
+    inputs from host, per-stream summaries back.
 
-    Pipeline edges: the first step chunk is short (chunk / 8) so the first
-    copy is short; with one D2H part the last chunk is short too (little
-    kernel time after the last copy); with many streams (``d2h_parts`` > 1, default one part per
-    131,072 streams, at most 8) the last chunk runs as stream-range launches
-    and each range's aggregate rows go device->host on a second copy stream while
-    the next range computes.  Back-to-back passes overlap: a pass's first
-    copies wait only for the previous pass's last use of each trace buffer,
-    so they run under its last chunks.  The returned tensor is ready once
-    the caller's current stream has synchronised (it waits on the copy
-    stream); a later pass rewrites it.
+    Pipeline edges: the first chunks ramp up from chunk / 8 so
+    the first copy is short; with one D2H part the last chunk is short too
+    (little kernel time after the last copy); with many streams
+    (``d2h_parts`` > 1, default one part per 131,072 streams, at most 8) the
+    last chunk runs as stream-range launches and each range's aggregate rows
+    go device->host on a second copy stream while the next range computes.
+    Back-to-back passes overlap: a pass's first copies wait only for the
+    previous pass's last use of each trace buffer.  The returned tensor is
+    ready once the caller's current stream has synchronised (it waits on the
+    D2H stream); a later pass rewrites it.
     """
 
     def __init__(self, space, specs, packed: PackedEnvs, policy: str = "alert", *, kalman=None,
@@ -281,6 +282,7 @@ class HostStreamer:
         # last use of each trace buffer by the previous pass: the next pass's first copies wait only for
         # these, so they run under the previous pass's last chunks (back-to-back passes keep PCIe busy)
         self._released = [None] * n_buffers
+        self._comp = None  # the compute stream of the last pass
         self.d2h_stream = torch.cuda.Stream(d)  # aggregate rows back, beside the H2D copies
         self.agg_host = torch.empty((self.n_streams, abi.AGG_FIELDS), dtype=torch.float64).pin_memory()
 
@@ -299,6 +301,9 @@ class HostStreamer:
         comp = torch.cuda.current_stream(eng.tdev)
         if self._released[0] is None:  # first pass: copies ordered after the caller's prior work
             self.copy_stream.wait_stream(comp)
+        elif self._comp is not None and self._comp != comp:  # the map / state of the last pass are in use there
+            comp.wait_stream(self._comp)
+        self._comp = comp
         for h, dv in zip(self.map_host, self.map_dev):
             dv.copy_(h, non_blocking=True)
         state = eng.new_state(self.table, self.n_streams, self.kalman, self.idle_cfg, init=False)

@@ -105,6 +105,12 @@ def test_host_streamer_matches_device_resident(c2):
         agg = hs.run()
         torch.cuda.current_stream().synchronize()
         np.testing.assert_array_equal(agg.numpy(), dev.agg)
+    side = torch.cuda.Stream()  # a pass issued from another caller stream, back to back with the last one
+    hs.run()
+    with torch.cuda.stream(side):
+        agg = hs.run()
+    side.synchronize()
+    np.testing.assert_array_equal(agg.numpy(), dev.agg)
 
 
 def test_host_streamer_stream_ranges_grid():
