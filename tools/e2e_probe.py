@@ -32,11 +32,11 @@ def timed(hs, reps=5):
 
 
 res = {}
-chunk = n_steps // 10
-for nb in (3, 2, 4, 2, 3):
+for div in (10, 20, 40, 10, 20):
+    chunk = n_steps // div
     hs = HostStreamer(wl["space"], wl["specs"], wl["packed"], "alert", stream_spec=wl["stream_spec"],
-                      stream_row=wl["stream_row"], chunk_steps=chunk, n_buffers=nb)
-    res[f"buffers{nb}_{len(res)}"] = timed(hs)
+                      stream_row=wl["stream_row"], chunk_steps=chunk)
+    res[f"chunk{chunk}_{len(res)}"] = timed(hs)
     del hs
     torch.cuda.empty_cache()
 print(json.dumps({"config": cfg, "streams": total, "steps": n_steps, "ms_per_pass": res}))
