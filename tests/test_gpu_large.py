@@ -210,3 +210,32 @@ def test_c4_grid_row_scan_equals_full_scan(lanes):
     np.testing.assert_array_equal(fast.decoded()["cand"], full.decoded()["cand"])
     np.testing.assert_array_equal(fast.records["energy"], full.records["energy"])
     np.testing.assert_array_equal(fast.agg[:, :abi.AGG_LEVEL0], full.agg[:, :abi.AGG_LEVEL0])
+
+
+@pytest.mark.parametrize("policy", ["alert+oracle", "alert-any"])
+def test_host_streamer_goal_changes_and_policies(policy):
+    """The host-streaming path with goal changes streamed beside the trace
+    (one launch over every spec per chunk), the oracle alongside, and a
+    kinds-filtered policy: per-stream aggregates equal the device-resident
+    run bit for bit."""
+    from paper_1911_00119_b200.simulator import HostStreamer
+    from paper_1911_00119_b200.trace import pack_goal_changes
+
+    space = A.preset_space()
+    ref = A.reference_latency(space)
+    specs = [A.ConstraintSpec(mode=A.Mode.MINIMIZE_ENERGY, t_goal=ref, q_goal=0.7, overhead_budget=0.01 * ref),
+             A.ConstraintSpec(mode=A.Mode.MAXIMIZE_ACCURACY, t_goal=0.8 * ref, e_goal=0.6 * 50 * 0.8 * ref,
+                              pr_threshold=0.95, overhead_budget=0.01 * ref),
+             A.ConstraintSpec(mode=A.Mode.MINIMIZE_ENERGY, t_goal=1.5 * ref, q_goal=0.85, overhead_budget=0.0)]
+    n, steps = 300, 600
+    packed = preset_batch(n, lengths=(200, 200, 200), seed0=77, dtype=np.float32, processes=1)
+    sched = [None if k % 5 == 0 else [(0, k % 3), (150 + k % 7, (k + 1) % 3), (420, (k + 2) % 3)]
+             for k in range(n)]
+    packed.goal_n, packed.goal_end, packed.goal_spec = pack_goal_changes(sched, steps, len(specs))
+    ps = A.pack_specs(specs)
+    ss = (np.arange(n) % len(specs)).astype(np.int32)
+    dev = A.run_batch(space, ps, packed, policy, stream_spec=ss)
+    hs = HostStreamer(space, ps, packed, policy, stream_spec=ss, chunk_steps=128, d2h_parts=2)
+    agg = hs.run()
+    torch.cuda.current_stream().synchronize()
+    np.testing.assert_array_equal(agg.numpy(), dev.agg)
