@@ -1231,6 +1231,10 @@ __device__ __forceinline__ bool fast_max_accuracy_flat(const DevTable& T, const 
     if (skip) nxt = (int)((w >> 16) & 0xFFu);
     const float key = out ? kInfF : pack_key(fmaxf(2.0f - acc, pen), w);
     if (key < p1) bi = i;
+    // a new P1 more than the tie cut below the old one: every earlier key is
+    // >= the old P1 > key + dcut >= the final cut, so their marks could only
+    // fail the near-tie pass's key check after a chain re-derivation (c3 +3%)
+    if (key + dcut < p1) mlo = mhi = 0u;
     p2 = fminf(p2, fmaxf(p1, key));
     p1 = fminf(p1, key);
     pd = p1 + dcut;
